@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""Benchmark of the RLT2 dual-ascent bound (BASELINE.json config 4: N=30 nug-shaped).
+
+One STEP = one pass of the whole hot path over the workload:
+qap_rlt2_fix(root) [a0 init] + qap_rlt2_bound(T=20) [a1 iteration 0 + 20 × a2..a6].
+value = dual-ascent iterations/s over all ranks (T·K·ranks / max-over-ranks device time).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the CPU oracle (oracle/, the plain C implementation written from
+the paper) on the host cores: one step = one dual-ascent iteration of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RLT2 dual-ascent iters/s and LAPs/s at N=30 (1/2/4/8 B200); B&B nodes/s"
+N_DEFAULT, T_ITERS, SEED = 30, 20, 1
+
+
+def n_stored(n):
+    return n * n * (n - 1) * (n - 1) // 2 * (n - 2) * (n - 2)
+
+
+def laps_per_iter(n):
+    return n * n * (n - 1) * (n - 1) // 2 + n * n + 1
+
+
+def workload_cfg(n, extra=None):
+    cfg = {"workload": f"nug{n}-shaped (grid {'x'.join(map(str, __import__('qapgen').grid_shape(n)))}, "
+                       f"seed {SEED}), RLT2 bound: init + iteration 0 + T={T_ITERS} iterations, K=0, UB=inf",
+           "N": n, "T": T_ITERS, "stored_D_entries": n_stored(n), "laps_per_iter": laps_per_iter(n),
+           "l2": "inputs larger than L2: D tensor %.2f GB >> 126 MB L2" % (n_stored(n) * 8 / 1e9)}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        rows = []
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                rows.append((float(f[0]), float(f[1]), f[2:6], float(f[6])))
+            except (ValueError, IndexError):
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r for r in rows if r[3] > 0] or rows
+        reasons = sorted({self.REASONS[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(loaded)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(kernel):
+    """dram read+write bytes per launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if kernel in d:
+            return d[kernel].get("dram_bytes_per_launch")
+    return None
+
+
+# ------------------------------------------------------------------------------------------
+def oracle_cpu_baseline(n, iters=1):
+    """The oracle as it stands, single thread: init + iteration 0 untimed, `iters`
+    dual-ascent iterations timed."""
+    import oracle
+    import qapgen
+    inst = qapgen.nug(n, SEED)
+    st = oracle.State(inst.F, inst.D)
+    st.iteration0()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        st.iteration()
+    dt = time.perf_counter() - t0
+    return {"value": iters / dt, "unit": "iters/s", "cores": 1, "kind": "oracle",
+            "sample": f"N={n} nug seed {SEED}: {iters} dual-ascent iteration(s) after an untimed "
+                      f"init + iteration 0; plain C oracle, 1 thread, {dt:.1f} s",
+            "laps_per_s": iters * laps_per_iter(n) / dt, "host_cpu": _cpu_name()}
+
+
+def _cpu_name():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    import qapgen
+    n = args.n
+    inst = qapgen.nug(n, SEED)
+    st = oracle.State(inst.F, inst.D)
+    st.iteration0()
+    for _ in range(args.warmup):
+        st.iteration()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        st.iteration()
+    dt = time.perf_counter() - t0
+    v = args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": workload_cfg(n, {"step": "one dual-ascent iteration (CPU oracle)",
+                                       "parallelism": "single host thread"}),
+            "laps_per_s": v * laps_per_iter(n),
+            "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
+                             "sample": f"N={n} nug seed {SEED}: {args.warmup} untimed + {args.steps} timed "
+                                       "dual-ascent iterations after an untimed init + iteration 0; 1 thread",
+                             "host_cpu": _cpu_name()},
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lap-warps", type=int, default=0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+
+    import paper_1510_02065_b200 as pkg
+    import qapgen
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n, T = args.n, T_ITERS
+    inst = qapgen.nug(n, SEED)
+    stream = torch.cuda.current_stream()
+    h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
+                            flags=pkg.QAP_FLAG_TIME_KERNELS, lap_warps=args.lap_warps)
+
+    def step():
+        pkg.qap_rlt2_fix(h, ())
+        return pkg.qap_rlt2_bound(h, T)
+
+    for _ in range(args.warmup):
+        step()
+    pkg.qap_rlt2_kernel_stats(h, reset=True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+            launches += r["launches"] + 1          # + k_init of fix
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ks = pkg.qap_rlt2_kernel_stats(h, reset=True)
+    lb = r["lb"]
+
+    # e2e through the public API with HOST buffers: create (H2D of F, D from pinned memory)
+    # + bound + result read-back + destroy, every step.
+    Fp = torch.from_numpy(inst.F).pin_memory()
+    Dp = torch.from_numpy(inst.D).pin_memory()
+    pkg.qap_destroy(h)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        h2 = pkg.qap_rlt2_create(n, Fp.numpy(), Dp.numpy(), device=local_rank, stream=stream.cuda_stream)
+        r2 = pkg.qap_rlt2_bound(h2, T)
+        pkg.qap_destroy(h2)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    if dist:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    assert r2["lb"] == lb, "e2e run must reproduce the device-resident bound bit for bit"
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    iters_total = T * args.steps * world
+    value = iters_total / (ms / 1e3)
+    peak, peak_src = measured_peaks()
+    per = {}
+    for k, v in ks.items():
+        if v["launches"]:
+            per[k] = {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
+                      "share": v["ms"] / max(1e-9, sum(x["ms"] for x in ks.values()))}
+    alg_bytes = 16 * n_stored(n)       # one read + one write of every stored D entry
+    dom = max(("lap2", "transfer"), key=lambda k: per.get(k, {}).get("share", 0))
+    achieved = alg_bytes / (per[dom]["avg_ms"] / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": {"lap2": "k_lap<1> (level-2 concentration)",
+                                       "transfer": "k_transfer"}[dom],
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": profiled_traffic(dom), "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
+    iter_ms = (per["sigma"]["avg_ms"] + per["transfer"]["avg_ms"] + per["lap2"]["avg_ms"]
+               + per["lap1"]["avg_ms"] * T / (T + 1) + per["lap0"]["avg_ms"])
+    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_cfg(n, {"parallelism": "replicas (one independent bound per GPU)" if world > 1
+                                       else "1 GPU"}),
+            "laps_per_s": value * laps_per_iter(n),
+            "lb": lb,
+            "effective_hbm": {"GB_per_s": alg_bytes * iters_total / world / (ms / 1e3) / 1e9,
+                              "frac": alg_bytes * iters_total / world / (ms / 1e3) / 1e9 / peak},
+            "kernels": per, "iter_kernel_ms": iter_ms,
+            "roofline": roof,
+            "e2e": {"value": T * e2e_steps * world / (ms_e2e / 1e3), "unit": "iters/s",
+                    "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 80,
+                    "path": "qap_rlt2_create(host F,D) + qap_rlt2_bound(T) + qap_destroy per step"},
+            "gpu_launches": launches,
+            "clocks": clk.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_cpu_baseline(n)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

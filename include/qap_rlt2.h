@@ -1,0 +1,195 @@
+/*
+ * qap_rlt2.h — C ABI of the B200 RLT2 dual-ascent lower-bound library (libqaprlt2.so).
+ *
+ * The library computes the level-2 RLT dual-ascent lower bound of a Koopmans–Beckmann
+ * QAP (Gonçalves et al., arXiv 1510.02065; P:n = /root/reference/PAPER.md line n):
+ *
+ *   min sum_{i,j,k!=i,n!=j} f_ik d_jn x_ij x_kn     over permutation matrices x
+ *
+ * by Algorithm 1: spread B->C->D, transfer between complementary costs of D,
+ * concentrate D->C, transfer C, concentrate C->B, concentrate B->LB, repeated.  Every
+ * concentration is an exact linear assignment problem whose residual replaces the
+ * submatrix.  All arithmetic runs in sm_100a CUDA kernels; the host code
+ * only sequences them.  Readings of the paper's silent points are DESIGN.md §3 R1..R30.
+ *
+ * Conventions
+ *   - Every function returns a qap_status; no exceptions cross the ABI.
+ *   - Pointers named *_dev are DEVICE pointers (current device); all others are HOST.
+ *   - Inputs are copied; the caller keeps ownership of everything it passes in.
+ *   - A handle is single-owner and not thread-safe (one worker at a time).
+ *   - All work is enqueued on opts->cuda_stream (NULL: the legacy default stream).
+ *     Calls that return host-visible results synchronise that stream.
+ *   - On failure, qap_last_error(h) returns a human-readable message.
+ *
+ * Export layouts (qap_rlt2_dual_copy; identical to the oracle's documented layout):
+ *   B : n×n row-major, b_ij
+ *   C : n² blocks C_ij in (i,j) row-major order; block (n-1)×(n-1) row-major; row k≠i
+ *       at index k-[k>i], column l≠j at index l-[l>j]
+ *   D : stored blocks D{ij,kl}, i<k, l≠j, in (i,j,k,l) lexicographic order; block
+ *       (n-2)×(n-2) row-major; row p∉{i,k} at p-[p>i]-[p>k], column q∉{j,l} at
+ *       q-[q>j]-[q>l].  D{kl,ij} is the same stored block ("complementary submatrices",
+ *       P:250-252) and each stored value equals both of its logical entries.
+ *   n is the number of FREE facilities at the current node (n = N at the root).
+ */
+#ifndef QAP_RLT2_H
+#define QAP_RLT2_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qap_rlt2 qap_rlt2;  /* opaque handle; owns all device memory it allocates */
+
+typedef enum {
+    QAP_OK = 0,
+    QAP_E_ARG = 1,       /* invalid argument (sizes, negative entries, bad partial assignment) */
+    QAP_E_CAPACITY = 2,  /* not enough device memory for N                                     */
+    QAP_E_CUDA = 3,      /* a CUDA runtime call failed                                          */
+    QAP_E_NCCL = 4,      /* reserved: multi-GPU communicator failure                            */
+    QAP_E_NUMERIC = 5,   /* a LAP residual fell below -tau (certificate failure, reading R8)    */
+    QAP_E_STATE = 6      /* call not valid in the handle's current state                         */
+} qap_status;
+
+typedef struct {
+    int32_t device;       /* CUDA device ordinal; -1 = current device                         */
+    void *cuda_stream;    /* cudaStream_t to enqueue on; NULL = legacy default stream          */
+    int32_t flags;        /* QAP_FLAG_* bit set                                                */
+    int32_t lap_warps;    /* warps per CTA of the level-2 LAP kernel; 0 = default              */
+} qap_rlt2_opts;
+
+#define QAP_FLAG_TIME_KERNELS 1   /* record CUDA events around every launch (qap_rlt2_kernel_stats) */
+
+typedef struct {
+    double lb;          /* kappa + dual bound after the last iteration run            */
+    double lb_glb;      /* bound after iteration 0 = Gilmore–Lawler (reading R1)               */
+    int32_t iters;      /* Algorithm-1 iterations run by this call (iteration 0 excluded)      */
+    int32_t status;     /* 0 iteration cap, 1 converged (LB'/UB < K), 2 pruned (LB > UB-1+1e-6) */
+    double *lb_trace;   /* optional HOST buffer: LB after each iteration of this call          */
+    int32_t lb_trace_cap;
+    int32_t launches;   /* kernels launched by this call                                       */
+} qap_rlt2_result;
+
+/*
+ * qap_rlt2_create — P:80-97 (flows f_ik, distances d_jn), P:179-181 (initial costs).
+ *   N   problem size, 3 <= N <= 64.
+ *   F   N×N row-major int64 flows  f_ik >= 0 (HOST; copied).
+ *   D   N×N row-major int64 distances d_jl >= 0 (HOST; copied).
+ *   Allocates the dual state for N (B, C and the halved D of P:250-252, ~8·N²(N-1)²(N-2)²/2
+ *   bytes) and initialises the root node (no fixed assignment), i.e. calls fix(h, 0, ...).
+ * Errors: QAP_E_ARG (N out of range, negative entry, N²·maxF·maxD >= 2^53 so that the
+ *   integer costs would not be exact in fp64); QAP_E_CAPACITY; QAP_E_CUDA.
+ */
+qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D,
+                           const qap_rlt2_opts *opts, qap_rlt2 **out);
+
+/*
+ * qap_rlt2_fix — set the node's partial assignment Φ = {(fac[t], loc[t]) : t < m}
+ *   (facility fac[t] at location loc[t]; HOST arrays of length m; m = 0 is the root).
+ *   REPLACES any previous Φ.  Rebuilds the reduced problem of the n = N-m free
+ *   facilities/locations (cold child, reading R19): b0 folds the fixed-free costs,
+ *   c_ij[kl] = f'_ik d'_jl, D = 0, LB = kappa (the fixed-fixed cost).  The next
+ *   qap_rlt2_bound starts with iteration 0.
+ * Errors: QAP_E_ARG (index out of range, duplicate facility or location, N-m < 3).
+ */
+qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_t *loc);
+
+/*
+ * qap_rlt2_bound — run Algorithm 1.
+ *   If the node is fresh (after create/fix), iteration 0 (concentrate C->B->LB, reading
+ *   R1) runs first; then up to max_iters iterations of the loop body P:185-193.  A later
+ *   call continues the ascent from the current dual state.
+ *   K   minimum relative progress (reading R14); 0 disables the test.
+ *   UB  upper bound (+INFINITY allowed; reading R15).  With UB finite the ascent stops
+ *       with status 2 when LB > UB - 1 + 1e-6 and with status 1 when K > 0 and
+ *       LB'/UB < K.  The stop test runs on the device after every iteration.
+ *   out (HOST, required) receives the bound; out->lb_trace may be NULL.
+ *   Synchronises the handle's stream.
+ * Errors: QAP_E_NUMERIC (LAP certificate failure), QAP_E_CUDA, QAP_E_ARG.
+ */
+qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB,
+                          qap_rlt2_result *out);
+
+/* Entry counts of the export layouts above for the current node (HOST outputs).       */
+qap_status qap_rlt2_dual_sizes(const qap_rlt2 *h, int64_t *nB, int64_t *nC, int64_t *nD);
+
+/*
+ * qap_rlt2_dual_copy — copy the dual state to HOST buffers in the export layouts above
+ *   (any of B, C, D may be NULL to skip).  Also returns kappa + accumulated dual (the
+ *   current LB) in *lb if lb != NULL.  Synchronises the handle's stream.
+ */
+qap_status qap_rlt2_dual_copy(const qap_rlt2 *h, double *B, double *C, double *D, double *lb);
+
+/*
+ * qap_rlt2_step — run ONE phase of an iteration (parity testing / profiling):
+ *   QAP_PHASE_ITER0       concentrate C->B, B->LB (reading R1)
+ *   QAP_PHASE_TRANSFER    spread B->C, spread C->D, transfer D
+ *   QAP_PHASE_CONC_D      concentrate D->C
+ *   QAP_PHASE_CONC_C      transfer C (exact no-op, reading R13) + concentrate C->B
+ *   QAP_PHASE_CONC_B      concentrate B->LB
+ * Phases must be called in Algorithm-1 order; otherwise QAP_E_STATE.
+ */
+#define QAP_PHASE_ITER0 0
+#define QAP_PHASE_TRANSFER 1
+#define QAP_PHASE_CONC_D 2
+#define QAP_PHASE_CONC_C 3
+#define QAP_PHASE_CONC_B 4
+qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase);
+
+/*
+ * qap_rlt2_kernel_stats — per-kernel launch counts and summed CUDA-event durations (ms)
+ *   recorded since the last reset, when the handle was created with
+ *   QAP_FLAG_TIME_KERNELS.  Kernel kinds: QAP_K_INIT, QAP_K_SIGMA, QAP_K_TRANSFER,
+ *   QAP_K_LAP2, QAP_K_LAP1, QAP_K_LAP0.  Arrays have QAP_K_COUNT entries (HOST).
+ *   reset != 0 clears the counters after reading.  Synchronises the stream.
+ */
+#define QAP_K_INIT 0
+#define QAP_K_SIGMA 1
+#define QAP_K_TRANSFER 2
+#define QAP_K_LAP2 3
+#define QAP_K_LAP1 4
+#define QAP_K_LAP0 5
+#define QAP_K_COUNT 6
+qap_status qap_rlt2_kernel_stats(qap_rlt2 *h, int64_t *launches, double *ms, int32_t reset);
+
+/* Last error message of h (or of the last failed create when h == NULL).             */
+const char *qap_last_error(const qap_rlt2 *h);
+
+/* Release the handle and its device memory; NULL-safe.                               */
+void qap_destroy(qap_rlt2 *h);
+
+/*
+ * qap_lap_batch — the batched warp LAP solver on its own (one warp per LAP,
+ *   P:243-245).  Solves `count` independent m×m problems M_b = M_dev + b*ld (DEVICE,
+ *   row-major, fp64, entries finite and >= 0), 1 <= m <= 64, ld >= m*m, ld even, M_dev
+ *   16-byte aligned.  Outputs (DEVICE, any may be NULL):
+ *     R_dev      + b*ld   residual (M - u) - v, clamped as in reading R8 (may alias M_dev)
+ *     S_dev      [b]      sum_r M[r][a(r)] in row order (reading R9)
+ *     assign_dev + b*m    column of each row (tie rule R6)
+ *     u_dev, v_dev + b*m  canonical duals (reading R5)
+ *     steps_dev  [b]      Dijkstra steps taken
+ *   Enqueued on `stream` (cudaStream_t, NULL = default); does not synchronise.  Returns
+ *   QAP_E_NUMERIC only from qap_lap_batch_status after a sync (status word per call).
+ */
+qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_dev,
+                         double *R_dev, double *S_dev, int32_t *assign_dev, double *u_dev,
+                         double *v_dev, int64_t *steps_dev, int32_t *err_dev, void *stream);
+
+/*
+ * qap_bnb_solve — minimal deterministic depth-first branch-and-bound (P:236-238 as the
+ *   caller of the bound).  Branches on the lowest-index free facility,
+ *   children in ascending location order; every node with n' >= 4 free facilities is
+ *   fixed (cold) and bounded with `iters` iterations; nodes with n' <= 3 are leaves
+ *   solved by enumeration; prune when LB > UB - 1 + 1e-6; the incumbent is replaced
+ *   only on strict improvement.  UB0 = +INFINITY for none.
+ *   Outputs (HOST): *opt (or -1 if nothing better than UB0), perm[N], node counts.
+ *   The handle's node is left at the last bounded node.
+ */
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int64_t *opt,
+                         int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QAP_RLT2_H */

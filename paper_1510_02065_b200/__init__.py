@@ -1,0 +1,237 @@
+"""Thin ctypes binding of libqaprlt2.so (include/qap_rlt2.h) — argument marshalling only.
+
+Every step of the RLT2 bound runs in the library's CUDA kernels.  There is no CPU
+fallback: if the shared library is missing or fails to load, importing the binding's
+functions raises.  Function names are the C ABI's names.
+
+    h = qap_rlt2_create(N, F, D)            # F, D: int64 N×N host arrays
+    r = qap_rlt2_bound(h, max_iters=20)     # dict(lb, lb_glb, iters, status, ...)
+    qap_rlt2_fix(h, [(fac, loc), ...])      # new node (cold)
+    B, C, D, lb = qap_rlt2_dual_copy(h)     # export layouts of include/qap_rlt2.h
+    qap_destroy(h)
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import math
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libqaprlt2.so")
+
+QAP_OK, QAP_E_ARG, QAP_E_CAPACITY, QAP_E_CUDA, QAP_E_NCCL, QAP_E_NUMERIC, QAP_E_STATE = range(7)
+STATUS_NAMES = ["OK", "E_ARG", "E_CAPACITY", "E_CUDA", "E_NCCL", "E_NUMERIC", "E_STATE"]
+QAP_FLAG_TIME_KERNELS = 1
+PHASE_ITER0, PHASE_TRANSFER, PHASE_CONC_D, PHASE_CONC_C, PHASE_CONC_B = range(5)
+KERNEL_KINDS = ["init", "sigma", "transfer", "lap2", "lap1", "lap0"]
+
+EXPORTS = ["qap_rlt2_create", "qap_rlt2_fix", "qap_rlt2_bound", "qap_rlt2_dual_sizes",
+           "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
+           "qap_destroy", "qap_lap_batch", "qap_bnb_solve"]
+
+
+class QapError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else status}: {msg}")
+        self.status = status
+
+
+class _Opts(ct.Structure):
+    _fields_ = [("device", ct.c_int32), ("cuda_stream", ct.c_void_p), ("flags", ct.c_int32),
+                ("lap_warps", ct.c_int32)]
+
+
+class _Result(ct.Structure):
+    _fields_ = [("lb", ct.c_double), ("lb_glb", ct.c_double), ("iters", ct.c_int32),
+                ("status", ct.c_int32), ("lb_trace", ct.POINTER(ct.c_double)),
+                ("lb_trace_cap", ct.c_int32), ("launches", ct.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libqaprlt2.so (fails loudly if absent: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -m paper_1510_02065_b200.build` "
+                          "(or __graft_entry__.build())")
+    L = ct.CDLL(path)
+    vp, i32, i64, f64 = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_double
+    L.qap_rlt2_create.argtypes = [i32, vp, vp, ct.POINTER(_Opts), ct.POINTER(vp)]
+    L.qap_rlt2_fix.argtypes = [vp, i32, vp, vp]
+    L.qap_rlt2_bound.argtypes = [vp, i32, f64, f64, ct.POINTER(_Result)]
+    L.qap_rlt2_dual_sizes.argtypes = [vp, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
+    L.qap_rlt2_dual_copy.argtypes = [vp, vp, vp, vp, ct.POINTER(f64)]
+    L.qap_rlt2_step.argtypes = [vp, i32]
+    L.qap_rlt2_kernel_stats.argtypes = [vp, vp, vp, i32]
+    L.qap_last_error.argtypes = [vp]
+    L.qap_last_error.restype = ct.c_char_p
+    L.qap_destroy.argtypes = [vp]
+    L.qap_destroy.restype = None
+    L.qap_lap_batch.argtypes = [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, ct.POINTER(i64), vp, ct.POINTER(i64),
+                                ct.POINTER(i64), ct.POINTER(i64)]
+    for name in EXPORTS:
+        if name not in ("qap_last_error", "qap_destroy"):
+            getattr(L, name).restype = ct.c_int
+    _lib = L
+    return L
+
+
+def _check(st: int, h=None):
+    if st != QAP_OK:
+        msg = load_library().qap_last_error(h.ptr if isinstance(h, Handle) else h)
+        raise QapError(st, (msg or b"").decode())
+
+
+def _current_stream():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+    except Exception:  # torch is plumbing only
+        pass
+    return None
+
+
+class Handle:
+    """Owner of a qap_rlt2* handle."""
+
+    def __init__(self, ptr, N: int):
+        self.ptr = ptr
+        self.N = N
+
+    def close(self):
+        if self.ptr:
+            load_library().qap_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0, lap_warps: int = 0) -> Handle:
+    L = load_library()
+    F = np.ascontiguousarray(F, dtype=np.int64)
+    D = np.ascontiguousarray(D, dtype=np.int64)
+    if F.shape != (N, N) or D.shape != (N, N):
+        raise ValueError("F and D must be N×N")
+    opts = _Opts(device, stream if stream is not None else _current_stream(), flags, lap_warps)
+    out = ct.c_void_p()
+    st = L.qap_rlt2_create(N, F.ctypes.data, D.ctypes.data, ct.byref(opts), ct.byref(out))
+    _check(st, None)
+    return Handle(out.value, N)
+
+
+def qap_rlt2_fix(h: Handle, fixed=()) -> None:
+    fac = np.array([a for a, _ in fixed] or [0], dtype=np.int32)
+    loc = np.array([b for _, b in fixed] or [0], dtype=np.int32)
+    _check(load_library().qap_rlt2_fix(h.ptr, len(fixed), fac.ctypes.data, loc.ctypes.data), h)
+
+
+def qap_rlt2_bound(h: Handle, max_iters: int, K: float = 0.0, UB: float = math.inf, trace: bool = False) -> dict:
+    r = _Result()
+    buf = None
+    if trace and max_iters > 0:
+        buf = (ct.c_double * max_iters)()
+        r.lb_trace = ct.cast(buf, ct.POINTER(ct.c_double))
+        r.lb_trace_cap = max_iters
+    _check(load_library().qap_rlt2_bound(h.ptr, max_iters, K, UB, ct.byref(r)), h)
+    out = dict(lb=r.lb, lb_glb=r.lb_glb, iters=r.iters, status=r.status, launches=r.launches)
+    if buf is not None:
+        out["trace"] = np.array(buf[: r.iters])
+    return out
+
+
+def qap_rlt2_dual_sizes(h: Handle):
+    a, b, c = ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(load_library().qap_rlt2_dual_sizes(h.ptr, ct.byref(a), ct.byref(b), ct.byref(c)), h)
+    return a.value, b.value, c.value
+
+
+def qap_rlt2_dual_copy(h: Handle, want_B=True, want_C=True, want_D=True):
+    nB, nC, nD = qap_rlt2_dual_sizes(h)
+    B = np.empty(nB) if want_B else None
+    C = np.empty(nC) if want_C else None
+    D = np.empty(nD) if want_D else None
+    lb = ct.c_double()
+    _check(load_library().qap_rlt2_dual_copy(h.ptr, None if B is None else B.ctypes.data,
+                                             None if C is None else C.ctypes.data,
+                                             None if D is None else D.ctypes.data, ct.byref(lb)), h)
+    return B, C, D, lb.value
+
+
+def qap_rlt2_step(h: Handle, phase: int) -> None:
+    _check(load_library().qap_rlt2_step(h.ptr, phase), h)
+
+
+def qap_rlt2_kernel_stats(h: Handle, reset: bool = False) -> dict:
+    n = len(KERNEL_KINDS)
+    launches = np.zeros(n, np.int64)
+    ms = np.zeros(n, np.float64)
+    _check(load_library().qap_rlt2_kernel_stats(h.ptr, launches.ctypes.data, ms.ctypes.data, int(reset)), h)
+    return {k: dict(launches=int(launches[i]), ms=float(ms[i])) for i, k in enumerate(KERNEL_KINDS)}
+
+
+def qap_destroy(h: Handle) -> None:
+    h.close()
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def qap_lap_batch(M, R=None, S=None, assign=None, u=None, v=None, steps=None, err=None, stream=None):
+    """Batched LAP on device tensors: M is (count, m, m) fp64 CUDA (torch) tensor; outputs
+    are preallocated CUDA tensors or None.  Enqueued on `stream` (default: current)."""
+    count, m, m2 = M.shape
+    if m != m2 or M.stride(2) != 1 or M.stride(1) != m:
+        raise ValueError("M must be (count, m, m) with row-major m×m matrices")
+    ld = M.stride(0)
+    st = load_library().qap_lap_batch(m, count, ld, _ptr(M), _ptr(R), _ptr(S), _ptr(assign), _ptr(u), _ptr(v),
+                                      _ptr(steps), _ptr(err), stream if stream is not None else _current_stream())
+    _check(st, None)
+
+
+def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf) -> dict:
+    opt = ct.c_int64()
+    perm = np.zeros(h.N, np.int32)
+    b, l, p = ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, ct.byref(opt), perm.ctypes.data, ct.byref(b),
+                                        ct.byref(l), ct.byref(p)), h)
+    return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value)
+
+
+class RLT2Bound:
+    """Convenience owner: RLT2Bound(inst_F, inst_D).bound(20)."""
+
+    def __init__(self, F, D, **kw):
+        F = np.asarray(F)
+        self.h = qap_rlt2_create(F.shape[0], F, D, **kw)
+
+    def fix(self, fixed=()):
+        qap_rlt2_fix(self.h, fixed)
+        return self
+
+    def bound(self, max_iters, K=0.0, UB=math.inf, trace=False):
+        return qap_rlt2_bound(self.h, max_iters, K, UB, trace)
+
+    def dual(self):
+        return qap_rlt2_dual_copy(self.h)
+
+    def close(self):
+        self.h.close()

@@ -1,0 +1,561 @@
+// rlt2_host.cu — host control of the RLT2 bound: the C ABI of include/qap_rlt2.h.
+//
+// The host only validates arguments, owns device memory and enqueues kernels in the
+// order of Algorithm 1; every arithmetic step of the bound runs on the GPU.
+// The stop test is evaluated on the device after each iteration and turns
+// the remaining launches of the call into no-ops, so a bound call synchronises once.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qap_rlt2.h"
+#include "rlt2_internal.h"
+
+using namespace rlt2;
+
+namespace {
+
+enum Phase { PH_FRESH = -1 };
+
+struct TimedLaunch {
+    int kind;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct qap_rlt2 {
+    int N = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int flags = 0;
+    int lap_warps = 0;
+    int num_sms = 148;
+    std::vector<int64_t> F, Dist;
+    int64_t *dF = nullptr, *dDist = nullptr;
+    double *dB = nullptr, *dC = nullptr, *dD = nullptr, *dSigma = nullptr, *dTrace = nullptr;
+    Ctl *dCtl = nullptr;
+    int trace_cap = 4096;
+    Node node{};
+    Geom geom{};
+    int next_phase = PH_FRESH;  // PH_FRESH: iteration 0 pending; else the next QAP_PHASE_*
+    int d_zero = 1, b_zero = 0, c_zero = 0;
+    std::string err;
+    // kernel timing (QAP_FLAG_TIME_KERNELS)
+    std::vector<TimedLaunch> pending;
+    std::vector<cudaEvent_t> pool;
+    int64_t launches[QAP_K_COUNT] = {0};
+    double ms[QAP_K_COUNT] = {0};
+    int call_launches = 0;
+};
+
+static std::string g_create_error;
+
+static qap_status fail(qap_rlt2 *h, qap_status st, const std::string &msg)
+{
+    if (h) h->err = msg; else g_create_error = msg;
+    return st;
+}
+
+static qap_status cuda_fail(qap_rlt2 *h, cudaError_t e, const char *where)
+{
+    return fail(h, QAP_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static cudaEvent_t ev_get(qap_rlt2 *h)
+{
+    if (!h->pool.empty()) {
+        cudaEvent_t e = h->pool.back();
+        h->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Enqueue one kernel through `fn`, bracketed by events when timing is on.
+template <class Fn>
+static cudaError_t launch(qap_rlt2 *h, int kind, Fn fn)
+{
+    cudaEvent_t a = nullptr, b = nullptr;
+    const bool timed = (h->flags & QAP_FLAG_TIME_KERNELS) != 0;
+    if (timed) {
+        a = ev_get(h);
+        b = ev_get(h);
+        cudaEventRecord(a, h->stream);
+    }
+    cudaError_t e = fn();
+    if (timed) {
+        cudaEventRecord(b, h->stream);
+        h->pending.push_back({kind, a, b});
+    }
+    h->call_launches++;
+    return e;
+}
+
+static void harvest_timing(qap_rlt2 *h)
+{
+    for (auto &t : h->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+            h->ms[t.kind] += ms;
+            h->launches[t.kind] += 1;
+        }
+        h->pool.push_back(t.a);
+        h->pool.push_back(t.b);
+    }
+    h->pending.clear();
+}
+
+static void free_all(qap_rlt2 *h)
+{
+    cudaFree(h->dF);
+    cudaFree(h->dDist);
+    cudaFree(h->dB);
+    cudaFree(h->dC);
+    cudaFree(h->dD);
+    cudaFree(h->dSigma);
+    cudaFree(h->dTrace);
+    cudaFree(h->dCtl);
+    for (auto &t : h->pending) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    for (auto e : h->pool) cudaEventDestroy(e);
+}
+
+extern "C" {
+
+qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
+                           qap_rlt2 **out)
+{
+    if (!out) return fail(nullptr, QAP_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (N < 3 || N > kMaxN) return fail(nullptr, QAP_E_ARG, "N must be in [3, 64]");
+    if (!F || !D) return fail(nullptr, QAP_E_ARG, "F or D is NULL");
+    int64_t maxf = 0, maxd = 0;
+    for (int64_t t = 0; t < (int64_t)N * N; t++) {
+        if (F[t] < 0 || D[t] < 0) return fail(nullptr, QAP_E_ARG, "negative flow or distance entry");
+        maxf = F[t] > maxf ? F[t] : maxf;
+        maxd = D[t] > maxd ? D[t] : maxd;
+    }
+    // exactness of integer costs in fp64: N^2 maxF maxD < 2^53
+    const long double bound = (long double)N * N * (long double)maxf * (long double)maxd;
+    if (bound >= 9007199254740992.0L) return fail(nullptr, QAP_E_ARG, "N^2*maxF*maxD >= 2^53");
+
+    qap_rlt2 *h = new qap_rlt2();
+    h->N = N;
+    h->flags = opts ? opts->flags : 0;
+    h->lap_warps = opts ? opts->lap_warps : 0;
+    h->stream = opts ? static_cast<cudaStream_t>(opts->cuda_stream) : nullptr;
+    cudaError_t e;
+    if (opts && opts->device >= 0) {
+        if ((e = cudaSetDevice(opts->device)) != cudaSuccess) {
+            qap_status s = cuda_fail(nullptr, e, "cudaSetDevice");
+            delete h;
+            return s;
+        }
+    }
+    cudaGetDevice(&h->device);
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->F.assign(F, F + (size_t)N * N);
+    h->Dist.assign(D, D + (size_t)N * N);
+
+    Geom gN;
+    make_geom(N, gN);
+    const size_t bytesD = (size_t)gN.nblk * gN.ld2 * 8;
+    const size_t bytesC = (size_t)N * N * gN.ldc * 8;
+    const size_t bytesB = (((size_t)N * N + 1) & ~size_t(1)) * 8;
+    const size_t bytesS = (size_t)gN.nblk * 8;
+    size_t freeb = 0, totb = 0;
+    if ((e = cudaMemGetInfo(&freeb, &totb)) != cudaSuccess) {
+        qap_status s = cuda_fail(nullptr, e, "cudaMemGetInfo");
+        delete h;
+        return s;
+    }
+    const size_t need = bytesD + bytesC + bytesB + bytesS + (64u << 20);
+    if (need > freeb) {
+        delete h;
+        char msg[160];
+        snprintf(msg, sizeof msg, "needs %.3f GB of device memory, %.3f GB free", need / 1e9, freeb / 1e9);
+        return fail(nullptr, QAP_E_CAPACITY, msg);
+    }
+#define ALLOC(ptr, bytes)                                                       \
+    if ((e = cudaMalloc(reinterpret_cast<void **>(&ptr), (bytes))) != cudaSuccess) { \
+        free_all(h);                                                            \
+        delete h;                                                               \
+        return e == cudaErrorMemoryAllocation ? fail(nullptr, QAP_E_CAPACITY, "cudaMalloc failed") \
+                                              : cuda_fail(nullptr, e, "cudaMalloc");  \
+    }
+    ALLOC(h->dF, (size_t)N * N * 8);
+    ALLOC(h->dDist, (size_t)N * N * 8);
+    ALLOC(h->dB, bytesB);
+    ALLOC(h->dC, bytesC);
+    ALLOC(h->dD, bytesD);
+    ALLOC(h->dSigma, bytesS);
+    ALLOC(h->dTrace, (size_t)h->trace_cap * 8);
+    ALLOC(h->dCtl, sizeof(Ctl));
+#undef ALLOC
+    if ((e = cudaMemcpyAsync(h->dF, F, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h->dDist, D, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->dCtl, 0, sizeof(Ctl), h->stream)) != cudaSuccess) {
+        free_all(h);
+        delete h;
+        return cuda_fail(nullptr, e, "upload");
+    }
+    qap_status s = qap_rlt2_fix(h, 0, nullptr, nullptr);
+    if (s != QAP_OK) {
+        g_create_error = h->err;
+        free_all(h);
+        delete h;
+        return s;
+    }
+    *out = h;
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_t *loc)
+{
+    if (!h) return QAP_E_ARG;
+    const int N = h->N;
+    if (m < 0 || N - m < 3) return fail(h, QAP_E_ARG, "need 0 <= m <= N-3");
+    if (m > 0 && (!fac || !loc)) return fail(h, QAP_E_ARG, "fac/loc NULL");
+    bool uf[kMaxN] = {false}, ul[kMaxN] = {false};
+    for (int t = 0; t < m; t++) {
+        if (fac[t] < 0 || fac[t] >= N || loc[t] < 0 || loc[t] >= N)
+            return fail(h, QAP_E_ARG, "fixed index out of range");
+        if (uf[fac[t]] || ul[loc[t]]) return fail(h, QAP_E_ARG, "duplicate facility or location in fixed set");
+        uf[fac[t]] = ul[loc[t]] = true;
+    }
+    Node nd{};
+    nd.N = N;
+    nd.m = m;
+    nd.n = N - m;
+    int a = 0, b = 0;
+    for (int x = 0; x < N; x++) {
+        if (!uf[x]) nd.I[a++] = x;
+        if (!ul[x]) nd.J[b++] = x;
+    }
+    for (int t = 0; t < m; t++) {
+        nd.fac[t] = fac[t];
+        nd.loc[t] = loc[t];
+    }
+    h->node = nd;
+    make_geom(nd.n, h->geom);
+    h->call_launches = 0;
+    cudaError_t e = launch(h, QAP_K_INIT, [&] {
+        return launch_init(h->node, h->geom, h->dF, h->dDist, h->dB, h->dC, h->dCtl, h->stream);
+    });
+    if (e != cudaSuccess) return cuda_fail(h, e, "k_init");
+    h->next_phase = PH_FRESH;
+    h->d_zero = 1;
+    h->b_zero = 0;
+    h->c_zero = 0;
+    return QAP_OK;
+}
+
+static cudaError_t run_phase(qap_rlt2 *h, int phase)
+{
+    cudaError_t e = cudaSuccess;
+    const Geom &g = h->geom;
+    switch (phase) {
+    case QAP_PHASE_ITER0:
+        e = launch(h, QAP_K_LAP1, [&] {
+            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, h->stream);
+        });
+        if (e) return e;
+        e = launch(h, QAP_K_LAP0, [&] {
+            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0,
+                                    h->stream);
+        });
+        break;
+    case QAP_PHASE_TRANSFER:
+        e = launch(h, QAP_K_SIGMA, [&] { return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->stream); });
+        if (e) return e;
+        e = launch(h, QAP_K_TRANSFER,
+                   [&] { return launch_transfer(g, h->dD, h->dSigma, h->d_zero, h->dCtl, h->stream); });
+        h->d_zero = 0;
+        h->b_zero = h->c_zero = 1;
+        break;
+    case QAP_PHASE_CONC_D:
+        e = launch(h, QAP_K_LAP2, [&] {
+            return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, h->lap_warps,
+                                    h->stream);
+        });
+        h->c_zero = 0;
+        break;
+    case QAP_PHASE_CONC_C:
+        // transfer between complementary costs of C: both members hold the same S after
+        // CONC_D, so the pair mean is an exact no-op (reading R13); then concentrate C->B.
+        e = launch(h, QAP_K_LAP1, [&] {
+            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, h->stream);
+        });
+        h->b_zero = 0;
+        break;
+    case QAP_PHASE_CONC_B:
+        e = launch(h, QAP_K_LAP0, [&] {
+            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, h->stream);
+        });
+        break;
+    default: return cudaErrorInvalidValue;
+    }
+    return e;
+}
+
+static qap_status read_ctl(qap_rlt2 *h, Ctl &c)
+{
+    cudaError_t e = cudaMemcpyAsync(&c, h->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "sync");
+    if (h->flags & QAP_FLAG_TIME_KERNELS) harvest_timing(h);
+    if (c.err) return fail(h, QAP_E_NUMERIC, "LAP residual below -tau (certificate failure)");
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase)
+{
+    if (!h) return QAP_E_ARG;
+    const int expect = h->next_phase == PH_FRESH ? QAP_PHASE_ITER0 : h->next_phase;
+    if (phase != expect) return fail(h, QAP_E_STATE, "phases must run in Algorithm-1 order");
+    h->call_launches = 0;
+    cudaError_t e = launch_ctl_begin(h->dCtl, 0.0, INFINITY, h->trace_cap, h->stream);
+    if (e == cudaSuccess) e = run_phase(h, phase);
+    if (e != cudaSuccess) return cuda_fail(h, e, "step");
+    h->next_phase = (phase == QAP_PHASE_CONC_B || phase == QAP_PHASE_ITER0) ? QAP_PHASE_TRANSFER : phase + 1;
+    Ctl c;
+    return read_ctl(h, c);
+}
+
+qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, qap_rlt2_result *out)
+{
+    if (!h || !out) return h ? fail(h, QAP_E_ARG, "out is NULL") : QAP_E_ARG;
+    if (max_iters < 0 || !(K >= 0.0) || std::isnan(UB)) return fail(h, QAP_E_ARG, "bad max_iters/K/UB");
+    if (h->next_phase != PH_FRESH && h->next_phase != QAP_PHASE_TRANSFER)
+        return fail(h, QAP_E_STATE, "bound called in the middle of an iteration");
+    if (max_iters > h->trace_cap) return fail(h, QAP_E_ARG, "max_iters above the trace capacity (4096)");
+    h->call_launches = 0;
+    cudaError_t e = launch_ctl_begin(h->dCtl, K, UB, h->trace_cap, h->stream);
+    h->call_launches++;
+    if (e != cudaSuccess) return cuda_fail(h, e, "ctl");
+    if (h->next_phase == PH_FRESH) {
+        if ((e = run_phase(h, QAP_PHASE_ITER0)) != cudaSuccess) return cuda_fail(h, e, "iteration 0");
+        h->next_phase = QAP_PHASE_TRANSFER;
+    }
+    for (int t = 0; t < max_iters; t++) {
+        for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_B; ph++)
+            if ((e = run_phase(h, ph)) != cudaSuccess) return cuda_fail(h, e, "iteration");
+    }
+    Ctl c;
+    qap_status s = read_ctl(h, c);
+    if (s != QAP_OK) return s;
+    out->lb = c.lb;
+    out->lb_glb = c.lb_glb;
+    out->iters = c.iters;
+    out->status = c.status;
+    out->launches = h->call_launches;
+    if (out->lb_trace && out->lb_trace_cap > 0 && c.iters > 0) {
+        const int cnt = c.iters < out->lb_trace_cap ? c.iters : out->lb_trace_cap;
+        e = cudaMemcpy(out->lb_trace, h->dTrace, (size_t)cnt * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(h, e, "trace copy");
+    }
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_dual_sizes(const qap_rlt2 *h, int64_t *nB, int64_t *nC, int64_t *nD)
+{
+    if (!h) return QAP_E_ARG;
+    const int64_t n = h->geom.n;
+    if (nB) *nB = n * n;
+    if (nC) *nC = n * n * (n - 1) * (n - 1);
+    if (nD) *nD = h->geom.nblk * (n - 2) * (n - 2);
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_dual_copy(const qap_rlt2 *hc, double *B, double *C, double *D, double *lb)
+{
+    qap_rlt2 *h = const_cast<qap_rlt2 *>(hc);
+    if (!h) return QAP_E_ARG;
+    const Geom &g = h->geom;
+    const int64_t n = g.n;
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "sync");
+    if (B) {
+        if (h->b_zero) memset(B, 0, (size_t)n * n * 8);
+        else if ((e = cudaMemcpy(B, h->dB, (size_t)n * n * 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return cuda_fail(h, e, "copy B");
+    }
+    if (C) {
+        const size_t w = (size_t)(n - 1) * (n - 1) * 8;
+        if (h->c_zero) memset(C, 0, w * n * n);
+        else if ((e = cudaMemcpy2D(C, w, h->dC, g.ldc * 8, w, n * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return cuda_fail(h, e, "copy C");
+    }
+    if (D) {
+        const size_t w = (size_t)(n - 2) * (n - 2) * 8;
+        if (h->d_zero) memset(D, 0, w * g.nblk);
+        else if ((e = cudaMemcpy2D(D, w, h->dD, g.ld2 * 8, w, g.nblk, cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return cuda_fail(h, e, "copy D");
+    }
+    if (lb) {
+        Ctl c;
+        if ((e = cudaMemcpy(&c, h->dCtl, sizeof(Ctl), cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return cuda_fail(h, e, "copy ctl");
+        *lb = c.lb;
+    }
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_kernel_stats(qap_rlt2 *h, int64_t *launches, double *ms, int32_t reset)
+{
+    if (!h) return QAP_E_ARG;
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "sync");
+    harvest_timing(h);
+    for (int k = 0; k < QAP_K_COUNT; k++) {
+        if (launches) launches[k] = h->launches[k];
+        if (ms) ms[k] = h->ms[k];
+        if (reset) {
+            h->launches[k] = 0;
+            h->ms[k] = 0;
+        }
+    }
+    return QAP_OK;
+}
+
+const char *qap_last_error(const qap_rlt2 *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+void qap_destroy(qap_rlt2 *h)
+{
+    if (!h) return;
+    cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+}
+
+qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_dev, double *R_dev, double *S_dev,
+                         int32_t *assign_dev, double *u_dev, double *v_dev, int64_t *steps_dev, int32_t *err_dev,
+                         void *stream)
+{
+    if (m < 1 || m > 64 || count < 0 || ld < (int64_t)m * m || (ld & 1) || !M_dev) return QAP_E_ARG;
+    if (reinterpret_cast<uintptr_t>(M_dev) & 15) return QAP_E_ARG;
+    if (count == 0) return QAP_OK;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    LapBatchOut o{R_dev, S_dev, u_dev, v_dev, assign_dev, steps_dev, err_dev};
+    cudaError_t e = launch_lap_batch(m, count, ld, M_dev, o, sms, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+        g_create_error = std::string("qap_lap_batch: ") + cudaGetErrorString(e);
+        return QAP_E_CUDA;
+    }
+    return QAP_OK;
+}
+
+// ---- minimal deterministic B&B (P:236-238 caller) ----------------------
+namespace {
+struct Bnb {
+    qap_rlt2 *h;
+    int N, iters;
+    double K, UB;
+    bool have;
+    int64_t best;
+    std::vector<int32_t> best_perm;
+    int64_t bounded = 0, leaves = 0, pruned = 0;
+    qap_status st = QAP_OK;
+
+    int64_t cost(const std::vector<int32_t> &perm) const
+    {
+        int64_t v = 0;
+        for (int i = 0; i < N; i++)
+            for (int k = 0; k < N; k++) v += h->F[i * N + k] * h->Dist[perm[i] * N + perm[k]];
+        return v;
+    }
+    void leaf(std::vector<int32_t> &perm, const std::vector<int> &ffac, const std::vector<int> &floc, int t,
+              std::vector<char> &used)
+    {
+        if (t == (int)ffac.size()) {
+            const int64_t v = cost(perm);
+            if (!have || v < best) {
+                best = v;
+                have = true;
+                best_perm = perm;
+                if ((double)v < UB) UB = (double)v;
+            }
+            return;
+        }
+        for (size_t x = 0; x < floc.size(); x++) {
+            if (used[x]) continue;
+            used[x] = 1;
+            perm[ffac[t]] = floc[x];
+            leaf(perm, ffac, floc, t + 1, used);
+            used[x] = 0;
+        }
+    }
+    void visit(std::vector<int32_t> &fac, std::vector<int32_t> &loc)
+    {
+        if (st != QAP_OK) return;
+        std::vector<char> uf(N, 0), ul(N, 0);
+        for (size_t t = 0; t < fac.size(); t++) uf[fac[t]] = ul[loc[t]] = 1;
+        std::vector<int> ffac, floc;
+        for (int x = 0; x < N; x++) {
+            if (!uf[x]) ffac.push_back(x);
+            if (!ul[x]) floc.push_back(x);
+        }
+        if (ffac.size() <= 3) {
+            leaves++;
+            std::vector<int32_t> perm(N, 0);
+            for (size_t t = 0; t < fac.size(); t++) perm[fac[t]] = loc[t];
+            std::vector<char> used(floc.size(), 0);
+            leaf(perm, ffac, floc, 0, used);
+            return;
+        }
+        if ((st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return;
+        qap_rlt2_result r{};
+        if ((st = qap_rlt2_bound(h, iters, K, UB, &r)) != QAP_OK) return;
+        bounded++;
+        if (r.lb > UB - 1.0 + 1e-6) {
+            pruned++;
+            return;
+        }
+        const int f = ffac[0];
+        for (int x : floc) {
+            fac.push_back(f);
+            loc.push_back(x);
+            visit(fac, loc);
+            fac.pop_back();
+            loc.pop_back();
+        }
+    }
+};
+}  // namespace
+
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int64_t *opt, int32_t *perm,
+                         int64_t *bounded, int64_t *leaves, int64_t *pruned)
+{
+    if (!h || !opt || !perm || iters < 0) return QAP_E_ARG;
+    Bnb b;
+    b.h = h;
+    b.N = h->N;
+    b.iters = iters;
+    b.K = K;
+    b.UB = UB0;
+    b.have = false;
+    b.best = -1;
+    std::vector<int32_t> fac, loc;
+    b.visit(fac, loc);
+    if (b.st != QAP_OK) return b.st;
+    *opt = b.have ? b.best : -1;
+    if (b.have)
+        for (int x = 0; x < b.N; x++) perm[x] = b.best_perm[x];
+    if (bounded) *bounded = b.bounded;
+    if (leaves) *leaves = b.leaves;
+    if (pruned) *pruned = b.pruned;
+    return QAP_OK;
+}
+
+}  // extern "C"

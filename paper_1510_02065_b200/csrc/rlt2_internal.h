@@ -1,0 +1,81 @@
+// rlt2_internal.h — device-state layout and kernel launchers shared by the CUDA kernels
+// (rlt2_kernels.cu) and the host control (rlt2_host.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rlt2 {
+
+constexpr int kMaxN = 64;
+
+// Device-resident control block of one bound (stop test of P:183/P:193 on the device).
+struct Ctl {
+    double lb_dual;    // sum of all level-0 concentration values (LB - kappa)
+    double lbprime;    // LB' of the last iteration
+    double lb;         // (double)kappa + lb_dual
+    double lb_glb;     // after iteration 0
+    double K, UB;      // stop parameters of the current bound call
+    long long kappa;   // fixed-fixed cost of the node (int64, exact)
+    int iters;         // iterations completed in the current bound call
+    int status;        // 0 cap, 1 converged, 2 pruned
+    int stopped;       // 1: remaining launches of this call are no-ops
+    int err;           // bit 0: LAP residual below -tau (reading R8)
+    int trace_cap;
+    int pad;
+};
+
+// Geometry of the reduced problem at the current node.
+struct Geom {
+    int n;             // free facilities
+    int64_t ldc;       // stride (doubles) of one C block: (n-1)^2 rounded up to even
+    int64_t ld2;       // stride (doubles) of one stored D block: (n-2)^2 rounded up to even
+    int64_t nblk;      // stored D blocks n^2 (n-1)^2 / 2
+    int64_t off[kMaxN + 1];  // first block id of facility i (canonical first facility)
+};
+
+// Partial assignment of the node, passed to k_init by value.
+struct Node {
+    int N, n, m;
+    int I[kMaxN], J[kMaxN];        // free facilities / locations ascending
+    int fac[kMaxN], loc[kMaxN];    // fixed pairs
+};
+
+inline void make_geom(int n, Geom &g)
+{
+    g.n = n;
+    int64_t c = (int64_t)(n - 1) * (n - 1), d = (int64_t)(n - 2) * (n - 2);
+    g.ldc = (c + 1) & ~int64_t(1);
+    g.ld2 = (d + 1) & ~int64_t(1);
+    g.nblk = (int64_t)n * n * (n - 1) * (n - 1) / 2;
+    int64_t acc = 0;
+    for (int i = 0; i <= n && i <= kMaxN; i++) {
+        g.off[i] = acc;
+        if (i < n) acc += (int64_t)n * (n - 1 - i) * (n - 1);
+    }
+}
+
+// LAP launch levels.
+enum LapLevel { LAP_L2 = 0, LAP_L1_ACC = 1, LAP_L1_SET = 2, LAP_L0_ITER0 = 3, LAP_L0 = 4, LAP_BATCH = 5 };
+
+struct LapBatchOut {
+    double *R, *S, *u, *v;
+    int32_t *assign;
+    int64_t *steps;
+    int32_t *err;
+};
+
+// ---- launchers (rlt2_kernels.cu) -----------------------------------------------------
+cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const int64_t *Dist,
+                        double *B, double *C, Ctl *ctl, cudaStream_t st);
+cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaStream_t st);
+cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double *sigma,
+                         const Ctl *ctl, cudaStream_t st);
+cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, int d_zero,
+                            const Ctl *ctl, cudaStream_t st);
+// Level-2 / level-1 / level-0 concentrations (one warp per LAP).
+cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B,
+                             Ctl *ctl, double *trace, int num_sms, int lap_warps, cudaStream_t st);
+cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M,
+                             const LapBatchOut &o, int num_sms, cudaStream_t st);
+
+}  // namespace rlt2
