@@ -60,6 +60,8 @@ typedef struct {
 } qap_rlt2_opts;
 
 #define QAP_FLAG_TIME_KERNELS 1   /* record CUDA events around every launch (qap_rlt2_kernel_stats) */
+#define QAP_FLAG_OVERLAP 2        /* run the D transfer and the level-2 LAPs concurrently on two
+                                     internal streams (experimental; default: one after the other) */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */
@@ -163,8 +165,10 @@ void qap_destroy(qap_rlt2 *h);
  * qap_lap_batch — the batched warp LAP solver on its own (one warp per LAP,
  *   P:243-245).  Solves `count` independent m×m problems M_b = M_dev + b*ld (DEVICE,
  *   row-major, fp64, entries finite and >= 0), 1 <= m <= 64, ld >= m*m, ld even, M_dev
- *   16-byte aligned.  Outputs (DEVICE, any may be NULL):
- *     R_dev      + b*ld   residual (M - u) - v, clamped as in reading R8 (may alias M_dev)
+ *   16-byte aligned.  Outputs (DEVICE; R_dev required and 16-byte aligned, the others
+ *   may be NULL):
+ *     R_dev      + b*ld   residual (M - u) - v, clamped as in reading R8 (may alias M_dev;
+ *                         the padding double of an odd m*m block may be overwritten)
  *     S_dev      [b]      sum_r M[r][a(r)] in row order (reading R9)
  *     assign_dev + b*m    column of each row (tie rule R6)
  *     u_dev, v_dev + b*m  canonical duals (reading R5)

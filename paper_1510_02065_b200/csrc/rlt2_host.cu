@@ -38,6 +38,10 @@ struct qap_rlt2 {
     std::vector<int64_t> F, Dist;
     int64_t *dF = nullptr, *dDist = nullptr;
     double *dB = nullptr, *dC = nullptr, *dD = nullptr, *dSigma = nullptr, *dTrace = nullptr;
+    int *dTriples = nullptr;
+    Sched *dSched = nullptr;
+    cudaStream_t sL = nullptr, sT = nullptr;  // LAP (high priority) / transfer (low priority)
+    cudaEvent_t evJoin = nullptr, evS = nullptr, evL = nullptr;
     Ctl *dCtl = nullptr;
     int trace_cap = 4096;
     Node node{};
@@ -78,25 +82,26 @@ static cudaEvent_t ev_get(qap_rlt2 *h)
     return e;
 }
 
-// Enqueue one kernel through `fn`, bracketed by events when timing is on.
+// Enqueue one kernel through `fn` on stream `st`, bracketed by events when timing is on.
 template <class Fn>
-static cudaError_t launch(qap_rlt2 *h, int kind, Fn fn)
+static cudaError_t launch(qap_rlt2 *h, int kind, cudaStream_t st, Fn fn)
 {
     cudaEvent_t a = nullptr, b = nullptr;
     const bool timed = (h->flags & QAP_FLAG_TIME_KERNELS) != 0;
     if (timed) {
         a = ev_get(h);
         b = ev_get(h);
-        cudaEventRecord(a, h->stream);
+        cudaEventRecord(a, st);
     }
-    cudaError_t e = fn();
+    cudaError_t e = fn(st);
     if (timed) {
-        cudaEventRecord(b, h->stream);
+        cudaEventRecord(b, st);
         h->pending.push_back({kind, a, b});
     }
     h->call_launches++;
     return e;
 }
+
 
 static void harvest_timing(qap_rlt2 *h)
 {
@@ -122,6 +127,13 @@ static void free_all(qap_rlt2 *h)
     cudaFree(h->dSigma);
     cudaFree(h->dTrace);
     cudaFree(h->dCtl);
+    cudaFree(h->dTriples);
+    cudaFree(h->dSched);
+    if (h->sL) cudaStreamDestroy(h->sL);
+    if (h->sT) cudaStreamDestroy(h->sT);
+    if (h->evJoin) cudaEventDestroy(h->evJoin);
+    if (h->evS) cudaEventDestroy(h->evS);
+    if (h->evL) cudaEventDestroy(h->evL);
     for (auto &t : h->pending) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
@@ -200,7 +212,21 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
     ALLOC(h->dSigma, bytesS);
     ALLOC(h->dTrace, (size_t)h->trace_cap * 8);
     ALLOC(h->dCtl, sizeof(Ctl));
-#undef ALLOC
+    ALLOC(h->dTriples, (size_t)N * (N - 1) * (N - 2) / 6 * sizeof(int) + 16);
+    ALLOC(h->dSched, sizeof(Sched));
+    {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if ((e = cudaStreamCreateWithPriority(&h->sL, cudaStreamNonBlocking, hi)) != cudaSuccess ||
+            (e = cudaStreamCreateWithPriority(&h->sT, cudaStreamNonBlocking, lo)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&h->evS, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&h->evL, cudaEventDisableTiming)) != cudaSuccess) {
+            free_all(h);
+            delete h;
+            return cuda_fail(nullptr, e, "streams");
+        }
+    }
     if ((e = cudaMemcpyAsync(h->dF, F, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess ||
         (e = cudaMemcpyAsync(h->dDist, D, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess ||
         (e = cudaMemsetAsync(h->dCtl, 0, sizeof(Ctl), h->stream)) != cudaSuccess) {
@@ -248,8 +274,8 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
     h->node = nd;
     make_geom(nd.n, h->geom);
     h->call_launches = 0;
-    cudaError_t e = launch(h, QAP_K_INIT, [&] {
-        return launch_init(h->node, h->geom, h->dF, h->dDist, h->dB, h->dC, h->dCtl, h->stream);
+    cudaError_t e = launch(h, QAP_K_INIT, h->stream, [&](cudaStream_t st) {
+        return launch_init(h->node, h->geom, h->dF, h->dDist, h->dB, h->dC, h->dTriples, h->dCtl, st);
     });
     if (e != cudaSuccess) return cuda_fail(h, e, "k_init");
     h->next_phase = PH_FRESH;
@@ -259,47 +285,79 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
     return QAP_OK;
 }
 
-static cudaError_t run_phase(qap_rlt2 *h, int phase)
+// Enqueue one phase of Algorithm 1.  `st` is the stream the call's work is ordered on.
+// In overlapped mode the TRANSFER phase runs on the low-priority stream sT and the level-2
+// LAP kernel (CONC_D) on the high-priority stream sL concurrently with it: LAP warps take
+// blocks in facility order and wait for the transfer of their facility on the device
+// (Sched counters).  Both join back into `st`.
+static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused)
 {
     cudaError_t e = cudaSuccess;
     const Geom &g = h->geom;
     switch (phase) {
     case QAP_PHASE_ITER0:
-        e = launch(h, QAP_K_LAP1, [&] {
-            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, h->stream);
+        e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
+            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         if (e) return e;
-        e = launch(h, QAP_K_LAP0, [&] {
-            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0,
-                                    h->stream);
+        e = launch(h, QAP_K_LAP0, st, [&](cudaStream_t s) {
+            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         break;
     case QAP_PHASE_TRANSFER:
-        e = launch(h, QAP_K_SIGMA, [&] { return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->stream); });
-        if (e) return e;
-        e = launch(h, QAP_K_TRANSFER,
-                   [&] { return launch_transfer(g, h->dD, h->dSigma, h->d_zero, h->dCtl, h->stream); });
-        h->d_zero = 0;
-        h->b_zero = h->c_zero = 1;
-        break;
-    case QAP_PHASE_CONC_D:
-        e = launch(h, QAP_K_LAP2, [&] {
-            return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, h->lap_warps,
-                                    h->stream);
+    case QAP_PHASE_CONC_D: {
+        // bound() enqueues TRANSFER and CONC_D together (fused = true) so that, with
+        // QAP_FLAG_OVERLAP, they run concurrently; qap_rlt2_step runs them one at a time.
+        const bool ov = fused && (h->flags & QAP_FLAG_OVERLAP) != 0;
+        cudaStream_t sT = ov ? h->sT : st, sL = ov ? h->sL : st;
+        if (phase == QAP_PHASE_TRANSFER) {
+            if (ov) {
+                if ((e = cudaEventRecord(h->evJoin, st)) != cudaSuccess) return e;
+                if ((e = cudaStreamWaitEvent(sT, h->evJoin, 0)) != cudaSuccess) return e;
+            }
+            e = launch(h, QAP_K_SIGMA, sT, [&](cudaStream_t s) {
+                return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->dSched, s);
+            });
+            if (e) return e;
+            if (ov) {
+                if ((e = cudaEventRecord(h->evS, sT)) != cudaSuccess) return e;
+                if ((e = cudaStreamWaitEvent(sL, h->evS, 0)) != cudaSuccess) return e;
+            }
+            e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {
+                return launch_transfer(g, h->dD, h->dSigma, h->dTriples, h->d_zero, h->dCtl, h->dSched, s);
+            });
+            if (e) return e;
+            h->d_zero = 0;
+            h->b_zero = h->c_zero = 1;
+            if (!fused) break;
+        }
+        // overlapped: at most 16 LAP warps per SM so that transfer CTAs stay co-resident
+        // (LAP warps spin on the transfer's progress counters; co-residency => progress)
+        int cfg = h->lap_warps;
+        if (ov) cfg = (cfg & ~0xf0ff) | ((cfg & 0xff) && (cfg & 0xff) < 16 ? (cfg & 0xff) : 16);
+        e = launch(h, QAP_K_LAP2, sL, [&](cudaStream_t s) {
+            return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, cfg, h->dSched,
+                                    s);
         });
+        if (e) return e;
+        if (ov) {  // LAP2 finishes after the transfer (it waited for every facility)
+            if ((e = cudaEventRecord(h->evL, sL)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(st, h->evL, 0)) != cudaSuccess) return e;
+        }
         h->c_zero = 0;
         break;
+    }
     case QAP_PHASE_CONC_C:
         // transfer between complementary costs of C: both members hold the same S after
         // CONC_D, so the pair mean is an exact no-op (reading R13); then concentrate C->B.
-        e = launch(h, QAP_K_LAP1, [&] {
-            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, h->stream);
+        e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
+            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         h->b_zero = 0;
         break;
     case QAP_PHASE_CONC_B:
-        e = launch(h, QAP_K_LAP0, [&] {
-            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, h->stream);
+        e = launch(h, QAP_K_LAP0, st, [&](cudaStream_t s) {
+            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         break;
     default: return cudaErrorInvalidValue;
@@ -324,7 +382,7 @@ qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase)
     if (phase != expect) return fail(h, QAP_E_STATE, "phases must run in Algorithm-1 order");
     h->call_launches = 0;
     cudaError_t e = launch_ctl_begin(h->dCtl, 0.0, INFINITY, h->trace_cap, h->stream);
-    if (e == cudaSuccess) e = run_phase(h, phase);
+    if (e == cudaSuccess) e = run_phase(h, phase, h->stream, false);
     if (e != cudaSuccess) return cuda_fail(h, e, "step");
     h->next_phase = (phase == QAP_PHASE_CONC_B || phase == QAP_PHASE_ITER0) ? QAP_PHASE_TRANSFER : phase + 1;
     Ctl c;
@@ -343,12 +401,14 @@ qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, q
     h->call_launches++;
     if (e != cudaSuccess) return cuda_fail(h, e, "ctl");
     if (h->next_phase == PH_FRESH) {
-        if ((e = run_phase(h, QAP_PHASE_ITER0)) != cudaSuccess) return cuda_fail(h, e, "iteration 0");
+        if ((e = run_phase(h, QAP_PHASE_ITER0, h->stream, true)) != cudaSuccess) return cuda_fail(h, e, "iteration 0");
         h->next_phase = QAP_PHASE_TRANSFER;
     }
     for (int t = 0; t < max_iters; t++) {
-        for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_B; ph++)
-            if ((e = run_phase(h, ph)) != cudaSuccess) return cuda_fail(h, e, "iteration");
+        for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_B; ph++) {
+            if (ph == QAP_PHASE_CONC_D) continue;  // enqueued together with TRANSFER
+            if ((e = run_phase(h, ph, h->stream, true)) != cudaSuccess) return cuda_fail(h, e, "iteration");
+        }
     }
     Ctl c;
     qap_status s = read_ctl(h, c);
@@ -441,8 +501,8 @@ qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_d
                          int32_t *assign_dev, double *u_dev, double *v_dev, int64_t *steps_dev, int32_t *err_dev,
                          void *stream)
 {
-    if (m < 1 || m > 64 || count < 0 || ld < (int64_t)m * m || (ld & 1) || !M_dev) return QAP_E_ARG;
-    if (reinterpret_cast<uintptr_t>(M_dev) & 15) return QAP_E_ARG;
+    if (m < 1 || m > 64 || count < 0 || ld < (int64_t)m * m || (ld & 1) || !M_dev || !R_dev) return QAP_E_ARG;
+    if ((reinterpret_cast<uintptr_t>(M_dev) | reinterpret_cast<uintptr_t>(R_dev)) & 15) return QAP_E_ARG;
     if (count == 0) return QAP_OK;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -24,6 +24,14 @@ struct Ctl {
     int pad;
 };
 
+// Cross-kernel schedule of one iteration (overlap of transfer and level-2 LAPs):
+// done[a] counts finished transfer CTAs whose facility triple has smallest facility a;
+// head is the level-2 LAP work queue.  Reset by k_sigma every iteration.
+struct Sched {
+    unsigned done[kMaxN];
+    unsigned long long head;
+};
+
 // Geometry of the reduced problem at the current node.
 struct Geom {
     int n;             // free facilities
@@ -66,15 +74,18 @@ struct LapBatchOut {
 
 // ---- launchers (rlt2_kernels.cu) -----------------------------------------------------
 cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const int64_t *Dist,
-                        double *B, double *C, Ctl *ctl, cudaStream_t st);
+                        double *B, double *C, int *triples, Ctl *ctl, cudaStream_t st);
 cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaStream_t st);
 cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double *sigma,
-                         const Ctl *ctl, cudaStream_t st);
-cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, int d_zero,
-                            const Ctl *ctl, cudaStream_t st);
+                         const Ctl *ctl, Sched *sched, cudaStream_t st);
+cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, const int *triples,
+                            int d_zero, const Ctl *ctl, Sched *sched, cudaStream_t st);
 // Level-2 / level-1 / level-0 concentrations (one warp per LAP).
+// sched != nullptr (level 2 only): blocks come from the Sched queue in facility order and
+// wait for the transfer of their facility (concurrent-kernel overlap).
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B,
-                             Ctl *ctl, double *trace, int num_sms, int lap_warps, cudaStream_t st);
+                             Ctl *ctl, double *trace, int num_sms, int lap_warps, Sched *sched,
+                             cudaStream_t st);
 cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M,
                              const LapBatchOut &o, int num_sms, cudaStream_t st);
 

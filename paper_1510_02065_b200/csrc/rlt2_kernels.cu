@@ -59,8 +59,9 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity)
 {
-    uint32_t done = 0;
+    uint32_t done = 0, spins = 0;
     while (!done) {
+        if (++spins > (1u << 28)) __trap();  // a lost TMA transaction: fail, never hang
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
             : "=r"(done)
@@ -68,6 +69,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity)
             : "memory");
     }
 }
+
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // Order-preserving map fp64 -> u64 (unsigned order == numeric order, -0 < +0).
 __device__ __forceinline__ uint64_t okey(double x)
@@ -91,37 +110,49 @@ __device__ __forceinline__ int64_t bid_of(const Geom &g, int i, int j, int k, in
 
 // ---------------------------------------------------------------------------------------
 // The warp LAP solver (reading R4/R5/R6).  Lane `lane` owns columns
-// c = lane + 32 t (t < CPL).  Per column: v (dual), ucol = u of the row matched to the
-// column, p (matched row, -1 free), minv / way / used of the current Dijkstra search.
-// The dummy column of the textbook formulation (holding the row being inserted) lives in
-// warp-uniform registers (ucur).  Every floating-point operation and its order equals the
-// written-out algorithm of DESIGN.md §3 (O2), so residuals are reproducible bit for bit.
+// c = lane + 32 t (t < CPL).  Per column, in registers: v (dual), ucol = u of the row
+// matched to the column, poff = byte offset of that row in the smem cost block (-1: free),
+// minv / way of the current Dijkstra search.  A settled ("used") column carries
+// minv = NaN: `cur < NaN` is false, NaN's order key sorts after every number, and
+// `NaN - delta` stays NaN, so the scan and the argmin need no used-test.  The dummy
+// column of the textbook formulation (holding the row being inserted) lives in
+// warp-uniform registers (ucur).  Every floating-point operation and its order is the
+// written-out algorithm of DESIGN.md §3 (O2), so results are reproducible bit for bit.
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
 template <int CPL>
-__device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const bool (&used)[CPL],
-                                            const int (&p)[CPL], int lane, int &j1, bool &j1free,
-                                            double &delta)
+__device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const int (&poff)[CPL], uint32_t freemask,
+                                            int &j1, bool &j1free, double &delta)
 {
     if (CPL == 1) {
-        const uint64_t key = used[0] ? ~0ull : okey(minv[0]);
-        const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
+        // min over the order key's high word; the low word only decides among equal high
+        // words (warp-uniform branch); then prefer a free column, then the lowest index.
+        const uint64_t key = okey(minv[0]);
+        const uint32_t hi = static_cast<uint32_t>(key >> 32);
         const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
-        const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
-        const bool tie = (hi == mhi) && (lo == mlo);
-        const uint32_t ft = __ballot_sync(FULL_MASK, tie && p[0] < 0);
-        const uint32_t at = __ballot_sync(FULL_MASK, tie);
-        j1 = __ffs(ft ? ft : at) - 1;
+        uint32_t bal = __ballot_sync(FULL_MASK, hi == mhi);
+        if (__popc(bal) > 1) {
+            const uint32_t lo = static_cast<uint32_t>(key);
+            const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
+            bal = __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
+        }
+        const uint32_t ft = bal & freemask;
+        j1 = __ffs(ft ? ft : bal) - 1;
         j1free = ft != 0;
-        delta = okey_inv((static_cast<uint64_t>(mhi) << 32) | mlo);
+        delta = __shfl_sync(FULL_MASK, minv[0], j1);
     } else {
         // lane-local best by (key, matched, t), then warp-wide
         uint64_t key = ~0ull;
-        int rank = 7;
+        int rank = 0xff;
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
-            const uint64_t k = used[t] ? ~0ull : okey(minv[t]);
-            const int r = (p[t] >= 0 ? CPL : 0) + t;
-            if (k < key || (k == key && r < rank)) { key = k; rank = r; }
+            const uint64_t k = okey(minv[t]);
+            const int r = (poff[t] >= 0 ? CPL : 0) + t;
+            if (k < key || (k == key && r < rank)) {
+                key = k;
+                rank = r;
+            }
         }
         const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
         const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
@@ -136,78 +167,77 @@ __device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const boo
     }
 }
 
-template <int CPL>
-__device__ __forceinline__ double sel_t(const double (&a)[CPL], int t)
-{
-    return (CPL == 1 || t == 0) ? a[0] : a[CPL - 1];
-}
-template <int CPL>
-__device__ __forceinline__ int sel_t(const int (&a)[CPL], int t)
+template <int CPL, class T>
+__device__ __forceinline__ T sel_t(const T (&a)[CPL], int t)
 {
     return (CPL == 1 || t == 0) ? a[0] : a[CPL - 1];
 }
 
+// Solve the m×m LAP whose row-major costs start at Mlane - lane (shared memory).
+// Outputs per owned column: poff (matched row × 8m bytes), v, ucol.
 template <int CPL>
-__device__ __forceinline__ void warp_lap_solve(const double *__restrict__ M, int m, int lane, int (&p)[CPL],
+__device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int lane, int (&poff)[CPL],
                                                double (&v)[CPL], double (&ucol)[CPL], int &steps)
 {
     double minv[CPL];
+    double du[CPL];  // 1.0 on settled columns, else 0.0: fma(delta, du, x) == x + delta exactly
     int way[CPL];
-    bool used[CPL];
+    const int rowb = m * 8;
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         v[t] = 0.0;
         ucol[t] = 0.0;
-        p[t] = -1;
+        poff[t] = -1;
         way[t] = -1;
     }
     for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
         double ucur = 0.0;         // u of row i = u[p[dummy]]
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
-            minv[t] = CUDART_INF;
-            used[t] = (lane + 32 * t) >= m;  // columns >= m never take part
+            minv[t] = (lane + 32 * t) < m ? CUDART_INF : qnan();
+            du[t] = 0.0;
         }
-        int j0 = -1, i0 = i;
+        int j0 = -1, i0off = i * rowb;
         double ui0 = 0.0;
         int jfree;
+        const uint32_t freemask = __ballot_sync(FULL_MASK, poff[0] < 0 && lane < m);  // CPL == 1 only
         while (true) {
-            const double *row = M + i0 * m;
+            const double *row = reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off);
 #pragma unroll
             for (int t = 0; t < CPL; t++) {
-                if (!used[t]) {
-                    const double cur = (row[lane + 32 * t] - ui0) - v[t];
-                    if (cur < minv[t]) {
-                        minv[t] = cur;
-                        way[t] = j0;
-                    }
+                const double cur = (row[32 * t] - ui0) - v[t];
+                if (cur < minv[t]) {  // false for settled columns (minv = NaN)
+                    minv[t] = cur;
+                    way[t] = j0;
                 }
             }
             int j1;
             bool j1free;
             double delta;
-            warp_argmin<CPL>(minv, used, p, lane, j1, j1free, delta);
-#pragma unroll
-            for (int t = 0; t < CPL; t++) {
-                if (used[t]) {
-                    ucol[t] += delta;
-                    v[t] -= delta;
-                } else {
-                    minv[t] -= delta;
-                }
-            }
+            warp_argmin<CPL>(minv, poff, freemask, j1, j1free, delta);
+            // next row to scan (used only if j1 is matched): fetched with the same lane group
+            // as delta; ucol[j1] is not touched by this step's update (j1 is not yet settled)
+            const int src = j1 & 31, tt = j1 >> 5;
+            const int nx_off = __shfl_sync(FULL_MASK, sel_t<CPL>(poff, tt), src);
+            const double nx_u = __shfl_sync(FULL_MASK, sel_t<CPL>(ucol, tt), src);
             ucur += delta;
 #pragma unroll
-            for (int t = 0; t < CPL; t++)
-                if (lane + 32 * t == j1) used[t] = true;
+            for (int t = 0; t < CPL; t++) {
+                minv[t] -= delta;                   // NaN stays NaN on settled columns
+                ucol[t] = fma(delta, du[t], ucol[t]);  // settled: u[p[j]] += delta (exact product)
+                v[t] = fma(-delta, du[t], v[t]);       // settled: v[j] -= delta
+                if (lane + 32 * t == j1) {  // settle column j1: only the high words change
+                    du[t] = __hiloint2double(0x3ff00000, __double2loint(du[t]));
+                    minv[t] = __hiloint2double(0x7ff80000, __double2loint(minv[t]));
+                }
+            }
             steps++;
             if (j1free) {
                 jfree = j1;
                 break;
             }
-            const int src = j1 & 31, tt = j1 >> 5;
-            i0 = __shfl_sync(FULL_MASK, sel_t<CPL>(p, tt), src);
-            ui0 = __shfl_sync(FULL_MASK, sel_t<CPL>(ucol, tt), src);
+            i0off = nx_off;
+            ui0 = nx_u;
             j0 = j1;
         }
         // augment along way[]: columns on the path take the row (and its u) of way[c]
@@ -226,14 +256,14 @@ __device__ __forceinline__ void warp_lap_solve(const double *__restrict__ M, int
         double uold[CPL];
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
-            pold[t] = p[t];
+            pold[t] = poff[t];
             uold[t] = ucol[t];
         }
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             const int w = way[t];
             const int wl = (w < 0 ? 0 : w) & 31, wt = w < 0 ? 0 : (w >> 5);
-            int np = i;
+            int np = i * rowb;
             double nu = ucur;
 #pragma unroll
             for (int s = 0; s < CPL; s++) {
@@ -245,45 +275,67 @@ __device__ __forceinline__ void warp_lap_solve(const double *__restrict__ M, int
                 }
             }
             if (onp[t]) {
-                p[t] = np;
+                poff[t] = np;
                 ucol[t] = nu;
             }
         }
     }
 }
 
-// Residual (reading R8) to global + primal value S (reading R9).  Returns S (all lanes)
-// and sets `bad` if some residual fell below -tau.
+// Residual (reading R8), written IN PLACE over the smem cost block, + primal value S
+// (reading R9).  Returns S (all lanes) and sets `bad` if some residual fell below -tau.
+// p[t] receives the matched row of each owned column.
 template <int CPL>
-__device__ __forceinline__ double warp_lap_epilogue(const double *__restrict__ M, int m, int lane,
-                                                    const int (&p)[CPL], const double (&v)[CPL],
-                                                    const double (&ucol)[CPL], double *urow, double *sel,
-                                                    double *__restrict__ R, bool &bad)
+__device__ __forceinline__ double warp_lap_epilogue(double *M, int m, int lane, const int (&poff)[CPL],
+                                                    int (&p)[CPL], const double (&v)[CPL],
+                                                    const double (&ucol)[CPL], double *urow, double *sel, bool &bad)
 {
+    const int rowb = m * 8;
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         const int c = lane + 32 * t;
+        p[t] = c < m ? poff[t] / rowb : -1;
         if (c < m) {
             urow[p[t]] = ucol[t];
             sel[p[t]] = M[p[t] * m + c];
         }
     }
     __syncwarp();
-    double mx = 0.0, mn = 0.0;
-    for (int r = 0; r < m; r++) {
-        const double ur = urow[r];
+    // A negative raw residual is rare (rounding only): then the exact tau test runs on a
+    // recomputation below, before the block is overwritten.
+    bool neg = false;
+#pragma unroll
+    for (int t = 0; t < CPL; t++) {
+        const int c = lane + 32 * t;
+        if (c < m) {
+            const double vc = v[t];
+#pragma unroll 4
+            for (int r = 0; r < m; r++) neg |= ((M[r * m + c] - urow[r]) - vc) < 0.0;
+        }
+    }
+    double mn = 0.0, mx = 0.0;
+    if (__any_sync(FULL_MASK, neg)) {
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             const int c = lane + 32 * t;
-            if (c < m) {
-                const double a = M[r * m + c];
-                mx = fmax(mx, fabs(a));
-                double x = (a - ur) - v[t];
-                mn = fmin(mn, x);
-                if (x < 0.0) x = 0.0;
-                if (p[t] == r) x = 0.0;
-                if (x == 0.0) x = 0.0;  // canonical +0
-                if (R != nullptr) R[r * m + c] = x;
+            if (c < m)
+                for (int r = 0; r < m; r++) {
+                    mx = fmax(mx, fabs(M[r * m + c]));
+                    mn = fmin(mn, (M[r * m + c] - urow[r]) - v[t]);
+                }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < CPL; t++) {
+        const int c = lane + 32 * t;
+        if (c < m) {
+            double *Mc = M + c;
+            const int pr = p[t];
+            const double vc = v[t];
+#pragma unroll 4
+            for (int r = 0; r < m; r++) {
+                const double x = (Mc[r * m] - urow[r]) - vc;
+                Mc[r * m] = (x > 0.0 && pr != r) ? x : 0.0;  // x <= 0 (incl. -0) or assigned -> +0
             }
         }
     }
@@ -298,13 +350,22 @@ __device__ __forceinline__ double warp_lap_epilogue(const double *__restrict__ M
     }
     const double tau = 1e-9 * fmax(1.0, mx);
     bad = mn < -tau;
+    fence_proxy_async();  // residual (generic-proxy writes) -> visible to the TMA store
     __syncwarp();
     return S;
 }
 
-// Shared-memory carve-up per warp: 2 × buffer (TMA destinations), urow[64], sel[64], 2 mbarriers.
-__host__ __device__ inline size_t lap_buf_bytes(int64_t ld) { return ((size_t)ld * 8 + 127) & ~size_t(127); }
-__host__ __device__ inline size_t lap_warp_smem(int64_t ld) { return 2 * lap_buf_bytes(ld) + 64 * 8 * 2 + 128; }
+// Shared memory per warp: NBUF cost buffers (TMA destinations; m*m doubles plus 32*CPL
+// doubles of padding so that every lane may load its column of any row unconditionally),
+// urow[m], sel[m], 2 mbarriers — packed tightly so that 32 warps fit one SM at m = 28.
+__host__ __device__ inline size_t lap_buf_bytes(int m, int cpl)
+{
+    return (((size_t)m * m + 32 * cpl) * 8 + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t lap_warp_smem(int m, int cpl, int nbuf)
+{
+    return nbuf * lap_buf_bytes(m, cpl) + (((size_t)2 * m * 8 + 15) & ~size_t(15)) + 16;
+}
 
 struct LapArgs {
     LapLevel lvl;
@@ -317,61 +378,123 @@ struct LapArgs {
     Ctl *ctl;
     double *trace;
     LapBatchOut bo;
+    Sched *sched;  // non-null: dynamic queue + wait for the transfer of each block's facility
+    int ntile3;    // transfer CTAs per facility triple
 };
 
-template <int CPL>
-__global__ void __launch_bounds__(256) k_lap(const LapArgs a)
+// First (canonical) facility of stored block b; `hint` only moves forward.
+__device__ __forceinline__ int facility_of(const Geom &g, int64_t b, int &hint)
+{
+    while (hint + 1 < g.n && b >= g.off[hint + 1]) hint++;
+    return hint;
+}
+
+// Lane 0 only: block until the transfer of every facility <= a has finished (acquire),
+// then order those generic-proxy writes before our async-proxy (TMA) reads.
+__device__ __forceinline__ void wait_transfer(const LapArgs &a_, int a, int &ready)
+{
+    const int n = a_.g.n;
+    unsigned spins = 0;
+    while (ready < a) {
+        const int x = ready + 1;
+        const unsigned total = (unsigned)a_.ntile3 * (unsigned)((n - 1 - x) * (n - 2 - x) / 2);
+        if (x > n - 3 || ld_acquire(&a_.sched->done[x]) >= total) {
+            ready++;
+            spins = 0;
+        } else {
+            __nanosleep(256);
+            if (++spins > (1u << 26)) __trap();  // ~20 s without progress: fail, never hang
+        }
+    }
+    fence_proxy_async_global();
+}
+
+template <int CPL, int NBUF>
+__global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
 {
     if (a.ctl != nullptr && a.ctl->stopped) return;
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem[];
     const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t bufb = lap_buf_bytes(a.ld);
-    unsigned char *base = smem + (size_t)warp * lap_warp_smem(a.ld);
-    double *buf[2] = {reinterpret_cast<double *>(base), reinterpret_cast<double *>(base + bufb)};
-    double *urow = reinterpret_cast<double *>(base + 2 * bufb);
-    double *sel = urow + 64;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sel + 64);
-
-    const int64_t nw = (int64_t)gridDim.x * wpc;
-    int64_t b = (int64_t)blockIdx.x * wpc + warp;
-    if (b >= a.count) return;
     const int m = a.m;
+    const size_t bufb = lap_buf_bytes(m, CPL);
+    unsigned char *wbase = smem + (size_t)warp * lap_warp_smem(m, CPL, NBUF);
+    double *urow = reinterpret_cast<double *>(wbase + NBUF * bufb);
+    double *sel = urow + m;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(wbase + NBUF * bufb + (((size_t)2 * m * 8 + 15) & ~size_t(15)));
+
+    const bool dyn = a.sched != nullptr;
+    constexpr int CH = 4;  // blocks per work-queue grab (dynamic mode)
+    const int64_t nw = (int64_t)gridDim.x * wpc;
+    int64_t b, cend;
+    if (dyn) {
+        int64_t c0 = 0;
+        if (lane == 0) c0 = (int64_t)atomicAdd(&a.sched->head, (unsigned long long)CH);
+        b = __shfl_sync(FULL_MASK, c0, 0);
+        cend = b + CH < a.count ? b + CH : a.count;
+    } else {
+        b = (int64_t)blockIdx.x * wpc + warp;
+        cend = a.count;
+    }
+    if (b >= a.count) return;
     const uint32_t bytes = (uint32_t)(((int64_t)m * m + 1) & ~int64_t(1)) * 8u;
+    int hint_load = 0, ready = -1;
     if (lane == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         fence_mbar_init();
+        if (dyn) wait_transfer(a, facility_of(a.g, b, hint_load), ready);
         mbar_expect_tx(&mbar[0], bytes);
-        tma_load_1d(buf[0], a.src + b * a.ld, bytes, &mbar[0]);
+        tma_load_1d(wbase, a.src + b * a.ld, bytes, &mbar[0]);
     }
     __syncwarp();
 
     int icur = 0;  // canonical first facility of block b (L2), advanced monotonically
     bool anybad = false;
-    for (int it = 0; b < a.count; b += nw, it++) {
-        const int64_t nb = b + nw;
-        if (lane == 0 && nb < a.count) {
-            fence_proxy_async();
-            mbar_expect_tx(&mbar[(it + 1) & 1], bytes);
-            tma_load_1d(buf[(it + 1) & 1], a.src + nb * a.ld, bytes, &mbar[(it + 1) & 1]);
+    for (int it = 0; b < a.count; it++) {
+        int64_t nb;  // next block of this warp
+        if (dyn) {
+            nb = b + 1;
+            if (nb >= cend) {
+                int64_t c0 = 0;
+                if (lane == 0) c0 = (int64_t)atomicAdd(&a.sched->head, (unsigned long long)CH);
+                nb = __shfl_sync(FULL_MASK, c0, 0);
+                cend = nb + CH < a.count ? nb + CH : a.count;
+            }
+        } else {
+            nb = b + nw;
         }
-        mbar_wait(&mbar[it & 1], (it >> 1) & 1);
-        const double *M = buf[it & 1];
+        const int slot = NBUF == 2 ? (it & 1) : 0;
+        if (NBUF == 2 && lane == 0 && nb < a.count) {
+            if (dyn) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
+            bulk_wait_read();  // the residual store out of the other buffer has read it
+            mbar_expect_tx(&mbar[slot ^ 1], bytes);
+            tma_load_1d(wbase + (slot ^ 1) * bufb, a.src + nb * a.ld, bytes, &mbar[slot ^ 1]);
+        }
+        mbar_wait(&mbar[slot], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
+        double *M = reinterpret_cast<double *>(wbase + slot * bufb);
 
-        int p[CPL];
+        int poff[CPL], p[CPL];
         double v[CPL], ucol[CPL];
         int steps = 0;
-        warp_lap_solve<CPL>(M, m, lane, p, v, ucol, steps);
+        warp_lap_solve<CPL>(M + lane, m, lane, poff, v, ucol, steps);
         bool bad;
-        const double S = warp_lap_epilogue<CPL>(M, m, lane, p, v, ucol, urow, sel,
-                                                 a.dst ? a.dst + b * a.ld : nullptr, bad);
+        const double S = warp_lap_epilogue<CPL>(M, m, lane, poff, p, v, ucol, urow, sel, bad);
         anybad |= bad;
+        if (lane == 0) {
+            tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global
+            if (NBUF == 1 && nb < a.count) {          // buffer free once the store has read it
+                if (dyn) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
+                bulk_wait_read();
+                mbar_expect_tx(&mbar[0], bytes);
+                tma_load_1d(wbase, a.src + nb * a.ld, bytes, &mbar[0]);
+            }
+        }
 
         if (lane == 0) {
             switch (a.lvl) {
             case LAP_L2: {  // credit S to both complementary coefficients (reading R12)
                 const Geom &g = a.g;
-                while (icur + 1 < g.n && b >= g.off[icur + 1]) icur++;
+                facility_of(g, b, icur);
                 const int n = g.n, n1 = n - 1;
                 int64_t rem = b - g.off[icur];
                 const int per_j = (n1 - icur) * n1;
@@ -434,7 +557,9 @@ __global__ void __launch_bounds__(256) k_lap(const LapArgs a)
             }
         }
         __syncwarp();
+        b = nb;
     }
+    if (lane == 0) bulk_wait_all();
     if (anybad && lane == 0) {
         if (a.ctl) atomicOr(&a.ctl->err, 1);
         if (a.bo.err) atomicOr(a.bo.err, 1);
@@ -446,8 +571,25 @@ __global__ void __launch_bounds__(256) k_lap(const LapArgs a)
 // kappa; D is NOT written (the next transfer reads it as zero).
 // ---------------------------------------------------------------------------------------
 __global__ void k_init(const Node nd, const Geom g, const int64_t *__restrict__ F,
-                       const int64_t *__restrict__ Dist, double *B, double *C, Ctl *ctl)
+                       const int64_t *__restrict__ Dist, double *B, double *C, int *triples, Ctl *ctl)
 {
+    {  // facility triples i<k<p in lexicographic order (the transfer kernel's grid.y)
+        const int n = nd.n;
+        const int ntri = n * (n - 1) * (n - 2) / 6;
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += gridDim.x * blockDim.x) {
+            int rem = t, i = 0;
+            while (rem >= (n - 1 - i) * (n - 2 - i) / 2) {
+                rem -= (n - 1 - i) * (n - 2 - i) / 2;
+                i++;
+            }
+            int k = i + 1;
+            while (rem >= n - 1 - k) {
+                rem -= n - 1 - k;
+                k++;
+            }
+            triples[t] = i | (k << 8) | ((k + 1 + rem) << 16);
+        }
+    }
     const int N = nd.N, n = nd.n, n1 = n - 1;
     const int64_t n4 = (int64_t)n * n * n * n;
     const int64_t tot = n4 + (int64_t)n * n;
@@ -499,9 +641,13 @@ __global__ void k_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap)
 // B and C are then logically zero; both are fully overwritten later in the iteration.
 // ---------------------------------------------------------------------------------------
 __global__ void k_sigma(const Geom g, const double *__restrict__ B, const double *__restrict__ C,
-                        double *__restrict__ sigma, const Ctl *ctl)
+                        double *__restrict__ sigma, const Ctl *ctl, Sched *sched)
 {
     if (ctl->stopped) return;
+    if (blockIdx.x == 0 && threadIdx.x < kMaxN) {
+        sched->done[threadIdx.x] = 0;
+        if (threadIdx.x == 0) sched->head = 0;
+    }
     const int n = g.n, n1 = n - 1;
     const int64_t n4 = (int64_t)n * n * n * n;
     const double div1 = (double)(n - 1), div2 = (double)(2 * (n - 2));
@@ -527,92 +673,108 @@ __global__ void k_sigma(const Geom g, const double *__restrict__ B, const double
 // ---------------------------------------------------------------------------------------
 constexpr int TT = 8;
 
-__global__ void __launch_bounds__(256) k_transfer(const Geom g, double *__restrict__ D,
-                                                  const double *__restrict__ sigma, int d_zero, const Ctl *ctl,
-                                                  int ntile)
+// Shared-memory index of element (x,y,z) of a tile view: rows padded to 9 doubles so
+// that the transposed reads of the mean phase are (nearly) bank-conflict free.
+__device__ __forceinline__ int tix(int x, int y, int z) { return x * (TT * (TT + 1)) + y * (TT + 1) + z; }
+
+__global__ void __launch_bounds__(256, 6) k_transfer(const Geom g, double *__restrict__ D,
+                                                     const double *__restrict__ sigma, const int *__restrict__ triples,
+                                                     int d_zero, const Ctl *ctl, Sched *sched, int ntile)
 {
     if (ctl->stopped) return;
-    __shared__ double s1[TT * TT * TT], s2[TT * TT * TT], s3[TT * TT * TT];
+    __shared__ double sv[3][TT * TT * (TT + 1)];  // the three member views of the tile's classes
+    __shared__ long long rbase[3][TT * TT];       // element index of each view row in D (-1: none)
+    __shared__ double rsig[3][TT * TT];           // spread amount sigma of the row's block
     const int n = g.n, m2 = n - 2;
     const int64_t ld2 = g.ld2;
-    int i = 0, k, p;
-    {
-        int rem = blockIdx.y;
-        while (true) {
-            const int c = (n - 1 - i) * (n - 2 - i) / 2;
-            if (rem < c) break;
-            rem -= c;
-            i++;
-        }
-        k = i + 1;
-        while (true) {
-            const int c = n - 1 - k;
-            if (rem < c) break;
-            rem -= c;
-            k++;
-        }
-        p = k + 1 + rem;
-    }
+    const int tri = triples[blockIdx.y];  // (i,k,p), i<k<p, packed by k_init
+    const int i = tri & 0xff, k = (tri >> 8) & 0xff, p = tri >> 16;
     const int tile = blockIdx.x;
     const int q0 = (tile % ntile) * TT, l0 = ((tile / ntile) % ntile) * TT, j0 = (tile / (ntile * ntile)) * TT;
+    const int tid = threadIdx.x;
 
-    for (int e = threadIdx.x; e < TT * TT * TT; e += blockDim.x) {
-        const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;
-        {  // view 1: (j,l,q) = (a,b,c); contiguous along q
-            const int j = j0 + a, l = l0 + b, q = q0 + c;
-            if (j < n && l < n && q < n && j != l && j != q && l != q) {
-                const int64_t bb = bid_of(g, i, j, k, l);
-                const double x = d_zero ? 0.0 : D[bb * ld2 + (int64_t)(p - 2) * m2 + (q - (q > j) - (q > l))];
-                s1[e] = x + sigma[bb];
-            }
+    // rows: view 0 = D{ij,kl} row p-2 (rows (j,l)); view 1 = D{ij,pq} row k-1 (rows (j,q));
+    //       view 2 = D{kl,pq} row i   (rows (l,q)).  sigma is fetched now, used after the
+    //       D loads are in flight.
+    double sg = 0.0;
+    if (tid < 3 * TT * TT) {
+        const int vw = tid >> 6, x = (tid >> 3) & 7, y = tid & 7;
+        int r0, r1;
+        if (vw == 0) { r0 = j0 + x; r1 = l0 + y; }
+        else if (vw == 1) { r0 = j0 + x; r1 = q0 + y; }
+        else { r0 = l0 + x; r1 = q0 + y; }
+        long long base = -1;
+        if (r0 < n && r1 < n && r0 != r1) {
+            int64_t bb, row;
+            if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; }
+            else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; }
+            else { bb = bid_of(g, k, r0, p, r1); row = i; }
+            base = bb * ld2 + row * m2;
+            sg = sigma[bb];
         }
-        {  // view 2: (j,q,l) = (a,b,c); contiguous along l
-            const int j = j0 + a, q = q0 + b, l = l0 + c;
-            if (j < n && l < n && q < n && j != l && j != q && l != q) {
-                const int64_t bb = bid_of(g, i, j, p, q);
-                const double x = d_zero ? 0.0 : D[bb * ld2 + (int64_t)(k - 1) * m2 + (l - (l > j) - (l > q))];
-                s2[e] = x + sigma[bb];
-            }
-        }
-        {  // view 3: (l,q,j) = (a,b,c); contiguous along j
-            const int l = l0 + a, q = q0 + b, j = j0 + c;
-            if (j < n && l < n && q < n && j != l && j != q && l != q) {
-                const int64_t bb = bid_of(g, k, l, p, q);
-                const double x = d_zero ? 0.0 : D[bb * ld2 + (int64_t)i * m2 + (j - (j > l) - (j > q))];
-                s3[e] = x + sigma[bb];
-            }
-        }
+        rbase[vw][tid & 63] = base;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < TT * TT * TT; e += blockDim.x) {
-        const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;  // (j,l,q) offsets
+
+    // load: element e = (x,y,z) of view vw is row (x,y), free index z (contiguous in D)
+    long long addr[2][3];
+    double val[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int e = tid + 256 * h;
+        const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
+#pragma unroll
+        for (int vw = 0; vw < 3; vw++) {
+            // (a, b) = the row's two locations, f = the free (column) location
+            const int a = (vw == 2 ? l0 : j0) + x;
+            const int b = (vw == 0 ? l0 : q0) + y;
+            const int f = (vw == 0 ? q0 : (vw == 1 ? l0 : j0)) + z;
+            const long long base = rbase[vw][e >> 3];
+            long long ad = -1;
+            if (base >= 0 && f < n && f != a && f != b) ad = base + (f - (f > a) - (f > b));
+            addr[h][vw] = ad;
+            val[h][vw] = (ad >= 0 && !d_zero) ? D[ad] : 0.0;
+        }
+    }
+    if (tid < 3 * TT * TT) rsig[tid >> 6][tid & 63] = sg;
+    __syncthreads();
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int e = tid + 256 * h;
+        const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
+#pragma unroll
+        for (int vw = 0; vw < 3; vw++) sv[vw][tix(x, y, z)] = val[h][vw] + rsig[vw][e >> 3];
+    }
+    __syncthreads();
+    // mean of each class (j,l,q): e1 = sv0[j][l][q], e2 = sv1[j][q][l], e3 = sv2[l][q][j]
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int e = tid + 256 * h;
+        const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;
         const int j = j0 + a, l = l0 + b, q = q0 + c;
         if (j < n && l < n && q < n && j != l && j != q && l != q) {
-            const int e1 = e, e2 = (a << 6) | (c << 3) | b, e3 = (b << 6) | (c << 3) | a;
-            const double mu = ((s1[e1] + s2[e2]) + s3[e3]) / 3.0;
-            s1[e1] = mu;
-            s2[e2] = mu;
-            s3[e3] = mu;
+            const int e1 = tix(a, b, c), e2 = tix(a, c, b), e3 = tix(b, c, a);
+            const double mu = ((sv[0][e1] + sv[1][e2]) + sv[2][e3]) / 3.0;
+            sv[0][e1] = mu;
+            sv[1][e2] = mu;
+            sv[2][e3] = mu;
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < TT * TT * TT; e += blockDim.x) {
-        const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;
-        {
-            const int j = j0 + a, l = l0 + b, q = q0 + c;
-            if (j < n && l < n && q < n && j != l && j != q && l != q)
-                D[bid_of(g, i, j, k, l) * ld2 + (int64_t)(p - 2) * m2 + (q - (q > j) - (q > l))] = s1[e];
-        }
-        {
-            const int j = j0 + a, q = q0 + b, l = l0 + c;
-            if (j < n && l < n && q < n && j != l && j != q && l != q)
-                D[bid_of(g, i, j, p, q) * ld2 + (int64_t)(k - 1) * m2 + (l - (l > j) - (l > q))] = s2[e];
-        }
-        {
-            const int l = l0 + a, q = q0 + b, j = j0 + c;
-            if (j < n && l < n && q < n && j != l && j != q && l != q)
-                D[bid_of(g, k, l, p, q) * ld2 + (int64_t)i * m2 + (j - (j > l) - (j > q))] = s3[e];
-        }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int e = tid + 256 * h;
+        const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
+#pragma unroll
+        for (int vw = 0; vw < 3; vw++)
+            if (addr[h][vw] >= 0) D[addr[h][vw]] = sv[vw][tix(x, y, z)];
+    }
+    // publish: this tile of facility i is final (release; LAP warps acquire done[i])
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(&sched->done[i], 1u);
     }
 }
 
@@ -620,12 +782,12 @@ __global__ void __launch_bounds__(256) k_transfer(const Geom g, double *__restri
 // Launchers
 // ---------------------------------------------------------------------------------------
 cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const int64_t *Dist, double *B,
-                        double *C, Ctl *ctl, cudaStream_t st)
+                        double *C, int *triples, Ctl *ctl, cudaStream_t st)
 {
     const int64_t tot = (int64_t)g.n * g.n * g.n * g.n + (int64_t)g.n * g.n;
     int blocks = (int)((tot + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_init<<<blocks, 256, 0, st>>>(node, g, F, Dist, B, C, ctl);
+    k_init<<<blocks, 256, 0, st>>>(node, g, F, Dist, B, C, triples, ctl);
     return cudaGetLastError();
 }
 
@@ -636,60 +798,64 @@ cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaS
 }
 
 cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double *sigma, const Ctl *ctl,
-                         cudaStream_t st)
+                         Sched *sched, cudaStream_t st)
 {
     const int64_t tot = (int64_t)g.n * g.n * g.n * g.n;
     int blocks = (int)((tot + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_sigma<<<blocks, 256, 0, st>>>(g, B, C, sigma, ctl);
+    k_sigma<<<blocks, 256, 0, st>>>(g, B, C, sigma, ctl, sched);
     return cudaGetLastError();
 }
 
-cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, int d_zero, const Ctl *ctl,
-                            cudaStream_t st)
+cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, const int *triples, int d_zero,
+                            const Ctl *ctl, Sched *sched, cudaStream_t st)
 {
     const int n = g.n;
     const int ntile = (n + TT - 1) / TT;
     const int ntri = n * (n - 1) * (n - 2) / 6;
     dim3 grid(ntile * ntile * ntile, ntri);
-    k_transfer<<<grid, 256, 0, st>>>(g, D, sigma, d_zero, ctl, ntile);
+    k_transfer<<<grid, 256, 0, st>>>(g, D, sigma, triples, d_zero, ctl, sched, ntile);
     return cudaGetLastError();
 }
 
-template <int CPL>
-static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, cudaStream_t st)
+template <int CPL, int NBUF>
+static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
 {
-    const size_t smem = lap_warp_smem(a.ld) * wpc;
-    cudaError_t e = cudaFuncSetAttribute(k_lap<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = lap_warp_smem(a.m, CPL, NBUF) * wpc;
+    cudaError_t e = cudaFuncSetAttribute(k_lap<CPL, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL>, 32 * wpc, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF>, 32 * wpc, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t want = (a.count + wpc - 1) / wpc;
-    const int64_t cap = (int64_t)num_sms * per_sm;
+    int64_t cap = (int64_t)num_sms * per_sm;
+    if (a.sched) cap = (int64_t)num_sms * (per_sm < ctas_per_sm ? per_sm : ctas_per_sm);
     const int grid = (int)(want < cap ? want : cap);
-    k_lap<CPL><<<grid, 32 * wpc, smem, st>>>(a);
+    k_lap<CPL, NBUF><<<grid, 32 * wpc, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-static int pick_wpc(int64_t ld, int requested)
+// lap_cfg: bits 0-7 = warps per CTA (0: default), bit 8 = double buffering,
+// bits 12-15 = CTAs per SM in dynamic (overlapped) mode (0: 1).
+static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cudaStream_t st)
 {
-    const size_t per = lap_warp_smem(ld);
-    int w = requested > 0 ? requested : 4;
-    while (w > 1 && per * w > 200 * 1024) w--;
-    return w;
-}
-
-static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int wpc, cudaStream_t st)
-{
-    if (a.m <= 32) return launch_lap_on<1>(a, num_sms, wpc, st);
-    if (a.m <= 64) return launch_lap_on<2>(a, num_sms, wpc, st);
-    return cudaErrorInvalidValue;
+    const int cpl = a.m <= 32 ? 1 : 2;
+    if (a.m > 64) return cudaErrorInvalidValue;
+    const int nbuf = (lap_cfg & 0x100) ? 2 : 1;
+    int wpc = lap_cfg & 0xff;
+    if (wpc <= 0) wpc = a.sched ? 32 : 8;
+    int cps = (lap_cfg >> 12) & 0xf;
+    if (cps <= 0) cps = 1;
+    const size_t cap = (size_t)226 * 1024 / (a.sched ? cps : 1);
+    while (wpc > 1 && lap_warp_smem(a.m, cpl, nbuf) * wpc > cap) wpc--;
+    if (cpl == 1)
+        return nbuf == 2 ? launch_lap_on<1, 2>(a, num_sms, wpc, cps, st) : launch_lap_on<1, 1>(a, num_sms, wpc, cps, st);
+    return nbuf == 2 ? launch_lap_on<2, 2>(a, num_sms, wpc, cps, st) : launch_lap_on<2, 1>(a, num_sms, wpc, cps, st);
 }
 
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B, Ctl *ctl,
-                             double *trace, int num_sms, int lap_warps, cudaStream_t st)
+                             double *trace, int num_sms, int lap_warps, Sched *sched, cudaStream_t st)
 {
     LapArgs a{};
     a.lvl = lvl;
@@ -703,12 +869,17 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
     switch (lvl) {
     case LAP_L2:
         a.m = n - 2; a.count = g.nblk; a.ld = g.ld2; a.src = D; a.dst = D;
-        wpc = pick_wpc(a.ld, lap_warps);
+        wpc = lap_warps;
+        a.sched = sched;
+        {
+            const int nt = (n + TT - 1) / TT;
+            a.ntile3 = nt * nt * nt;
+        }
         break;
     case LAP_L1_ACC:
     case LAP_L1_SET:
         a.m = n - 1; a.count = (int64_t)n * n; a.ld = g.ldc; a.src = C; a.dst = C;
-        wpc = pick_wpc(a.ld, 2);
+        wpc = 1;
         break;
     case LAP_L0_ITER0:
     case LAP_L0:
@@ -732,7 +903,7 @@ cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M, 
     a.dst = o.R;
     a.bo = o;
     a.ctl = nullptr;
-    return dispatch_lap(a, num_sms, pick_wpc(ld, 4), st);
+    return dispatch_lap(a, num_sms, 2, st);
 }
 
 }  // namespace rlt2
