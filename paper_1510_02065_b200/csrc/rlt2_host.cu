@@ -297,11 +297,11 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
     switch (phase) {
     case QAP_PHASE_ITER0:
         e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
+            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
         });
         if (e) return e;
         e = launch(h, QAP_K_LAP0, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
+            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
         });
         break;
     case QAP_PHASE_TRANSFER:
@@ -324,7 +324,7 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
                 if ((e = cudaStreamWaitEvent(sL, h->evS, 0)) != cudaSuccess) return e;
             }
             e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {
-                return launch_transfer(g, h->dD, h->dSigma, h->dTriples, h->d_zero, h->dCtl, h->dSched, s);
+                return launch_transfer(g, h->dD, h->dSigma, h->dTriples, h->d_zero, h->dCtl, h->dSched, ov ? 1 : 0, s);
             });
             if (e) return e;
             h->d_zero = 0;
@@ -337,7 +337,7 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
         if (ov) cfg = (cfg & ~0xf0ff) | ((cfg & 0xff) && (cfg & 0xff) < 16 ? (cfg & 0xff) : 16);
         e = launch(h, QAP_K_LAP2, sL, [&](cudaStream_t s) {
             return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, cfg, h->dSched,
-                                    s);
+                                    ov ? 1 : 0, s);
         });
         if (e) return e;
         if (ov) {  // LAP2 finishes after the transfer (it waited for every facility)
@@ -351,13 +351,13 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
         // transfer between complementary costs of C: both members hold the same S after
         // CONC_D, so the pair mean is an exact no-op (reading R13); then concentrate C->B.
         e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
+            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
         });
         h->b_zero = 0;
         break;
     case QAP_PHASE_CONC_B:
         e = launch(h, QAP_K_LAP0, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
+            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
         });
         break;
     default: return cudaErrorInvalidValue;

@@ -79,13 +79,13 @@ cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaS
 cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double *sigma,
                          const Ctl *ctl, Sched *sched, cudaStream_t st);
 cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, const int *triples,
-                            int d_zero, const Ctl *ctl, Sched *sched, cudaStream_t st);
+                            int d_zero, const Ctl *ctl, Sched *sched, int publish, cudaStream_t st);
 // Level-2 / level-1 / level-0 concentrations (one warp per LAP).
 // sched != nullptr (level 2 only): blocks come from the Sched queue in facility order and
 // wait for the transfer of their facility (concurrent-kernel overlap).
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B,
                              Ctl *ctl, double *trace, int num_sms, int lap_warps, Sched *sched,
-                             cudaStream_t st);
+                             int wait, cudaStream_t st);
 cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M,
                              const LapBatchOut &o, int num_sms, cudaStream_t st);
 

@@ -496,12 +496,12 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
                 const Geom &g = a.g;
                 facility_of(g, b, icur);
                 const int n = g.n, n1 = n - 1;
-                int64_t rem = b - g.off[icur];
+                int rem = (int)(b - g.off[icur]);  // < n (n-1)^2: 32-bit divisions only
                 const int per_j = (n1 - icur) * n1;
-                const int j = (int)(rem / per_j);
-                rem -= (int64_t)j * per_j;
-                const int kk = (int)(rem / n1);
-                const int li = (int)(rem - (int64_t)kk * n1);
+                const int j = rem / per_j;
+                rem -= j * per_j;
+                const int kk = rem / n1;
+                const int li = rem - kk * n1;
                 const int i = icur, k = i + 1 + kk, l = li + (li >= j);
                 // C was spread to D and zeroed: c <- 0 + S = S.
                 a.C[(int64_t)(i * n + j) * g.ldc + (k - 1) * n1 + (l - (l > j))] = S;
@@ -676,21 +676,23 @@ constexpr int TT = 8;
 // Shared-memory index of element (x,y,z) of a tile view: rows padded to 9 doubles so
 // that the transposed reads of the mean phase are (nearly) bank-conflict free.
 __device__ __forceinline__ int tix(int x, int y, int z) { return x * (TT * (TT + 1)) + y * (TT + 1) + z; }
+constexpr unsigned NOIDX = 0xffffffffu;
 
-__global__ void __launch_bounds__(256, 6) k_transfer(const Geom g, double *__restrict__ D,
+__global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__restrict__ D,
                                                      const double *__restrict__ sigma, const int *__restrict__ triples,
-                                                     int d_zero, const Ctl *ctl, Sched *sched, int ntile)
+                                                     int d_zero, const Ctl *ctl, Sched *sched, int ntile, int publish)
 {
     if (ctl->stopped) return;
     __shared__ double sv[3][TT * TT * (TT + 1)];  // the three member views of the tile's classes
-    __shared__ long long rbase[3][TT * TT];       // element index of each view row in D (-1: none)
+    __shared__ unsigned rbase[3][TT * TT];        // element index of each view row in D (NOIDX: none)
     __shared__ double rsig[3][TT * TT];           // spread amount sigma of the row's block
     const int n = g.n, m2 = n - 2;
     const int64_t ld2 = g.ld2;
     const int tri = triples[blockIdx.y];  // (i,k,p), i<k<p, packed by k_init
     const int i = tri & 0xff, k = (tri >> 8) & 0xff, p = tri >> 16;
     const int tile = blockIdx.x;
-    const int q0 = (tile % ntile) * TT, l0 = ((tile / ntile) % ntile) * TT, j0 = (tile / (ntile * ntile)) * TT;
+    const int tl = tile / ntile, tj = tl / ntile;
+    const int q0 = (tile - tl * ntile) * TT, l0 = (tl - tj * ntile) * TT, j0 = tj * TT;
     const int tid = threadIdx.x;
 
     // rows: view 0 = D{ij,kl} row p-2 (rows (j,l)); view 1 = D{ij,pq} row k-1 (rows (j,q));
@@ -703,13 +705,14 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const Geom g, double *__res
         if (vw == 0) { r0 = j0 + x; r1 = l0 + y; }
         else if (vw == 1) { r0 = j0 + x; r1 = q0 + y; }
         else { r0 = l0 + x; r1 = q0 + y; }
-        long long base = -1;
+        unsigned base = NOIDX;
         if (r0 < n && r1 < n && r0 != r1) {
-            int64_t bb, row;
+            int64_t bb;
+            int row;
             if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; }
             else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; }
             else { bb = bid_of(g, k, r0, p, r1); row = i; }
-            base = bb * ld2 + row * m2;
+            base = (unsigned)(bb * ld2 + row * m2);
             sg = sigma[bb];
         }
         rbase[vw][tid & 63] = base;
@@ -717,7 +720,7 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const Geom g, double *__res
     __syncthreads();
 
     // load: element e = (x,y,z) of view vw is row (x,y), free index z (contiguous in D)
-    long long addr[2][3];
+    unsigned addr[2][3];
     double val[2][3];
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -729,11 +732,11 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const Geom g, double *__res
             const int a = (vw == 2 ? l0 : j0) + x;
             const int b = (vw == 0 ? l0 : q0) + y;
             const int f = (vw == 0 ? q0 : (vw == 1 ? l0 : j0)) + z;
-            const long long base = rbase[vw][e >> 3];
-            long long ad = -1;
-            if (base >= 0 && f < n && f != a && f != b) ad = base + (f - (f > a) - (f > b));
+            const unsigned base = rbase[vw][e >> 3];
+            unsigned ad = NOIDX;
+            if (base != NOIDX && f < n && f != a && f != b) ad = base + (unsigned)(f - (f > a) - (f > b));
             addr[h][vw] = ad;
-            val[h][vw] = (ad >= 0 && !d_zero) ? D[ad] : 0.0;
+            val[h][vw] = (ad != NOIDX && !d_zero) ? D[ad] : 0.0;
         }
     }
     if (tid < 3 * TT * TT) rsig[tid >> 6][tid & 63] = sg;
@@ -767,14 +770,15 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const Geom g, double *__res
         const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
 #pragma unroll
         for (int vw = 0; vw < 3; vw++)
-            if (addr[h][vw] >= 0) D[addr[h][vw]] = sv[vw][tix(x, y, z)];
+            if (addr[h][vw] != NOIDX) D[addr[h][vw]] = sv[vw][tix(x, y, z)];
     }
-    // publish: this tile of facility i is final (release; LAP warps acquire done[i])
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
+    if (publish) {  // overlapped mode: this tile of facility i is final (release)
         __threadfence();
-        atomicAdd(&sched->done[i], 1u);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(&sched->done[i], 1u);
+        }
     }
 }
 
@@ -808,13 +812,13 @@ cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double
 }
 
 cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, const int *triples, int d_zero,
-                            const Ctl *ctl, Sched *sched, cudaStream_t st)
+                            const Ctl *ctl, Sched *sched, int publish, cudaStream_t st)
 {
     const int n = g.n;
     const int ntile = (n + TT - 1) / TT;
     const int ntri = n * (n - 1) * (n - 2) / 6;
     dim3 grid(ntile * ntile * ntile, ntri);
-    k_transfer<<<grid, 256, 0, st>>>(g, D, sigma, triples, d_zero, ctl, sched, ntile);
+    k_transfer<<<grid, 256, 0, st>>>(g, D, sigma, triples, d_zero, ctl, sched, ntile, publish);
     return cudaGetLastError();
 }
 
@@ -855,7 +859,7 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
 }
 
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B, Ctl *ctl,
-                             double *trace, int num_sms, int lap_warps, Sched *sched, cudaStream_t st)
+                             double *trace, int num_sms, int lap_warps, Sched *sched, int wait, cudaStream_t st)
 {
     LapArgs a{};
     a.lvl = lvl;
@@ -873,7 +877,7 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
         a.sched = sched;
         {
             const int nt = (n + TT - 1) / TT;
-            a.ntile3 = nt * nt * nt;
+            a.ntile3 = wait ? nt * nt * nt : 0;  // 0: the transfer already completed (no waits)
         }
         break;
     case LAP_L1_ACC:
