@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "RLT2 dual-ascent iters/s and LAPs/s at N=30 (1/2/4/8 B200); B&B nodes/s"
 N_DEFAULT, T_ITERS, SEED = 30, 20, 1
+BNB_ITERS = 10
 
 
 def n_stored(n):
@@ -183,6 +184,7 @@ def main():
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lap-warps", type=int, default=0)
+    ap.add_argument("--no-bnb", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -235,21 +237,20 @@ def main():
     ks = pkg.qap_rlt2_kernel_stats(h, reset=True)
     lb = r["lb"]
 
-    # e2e through the public API with HOST buffers: create (H2D of F, D from pinned memory)
-    # + bound + result read-back + destroy, every step.
+    # e2e through the public API with HOST buffers: every step copies the instance (F, D)
+    # from pinned host memory into the handle (qap_rlt2_load = H2D + root init), runs the
+    # bound and reads the result back (D2H of the device control block).
     Fp = torch.from_numpy(inst.F).pin_memory()
     Dp = torch.from_numpy(inst.D).pin_memory()
-    pkg.qap_destroy(h)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, args.steps)
     for _ in range(e2e_steps):
-        h2 = pkg.qap_rlt2_create(n, Fp.numpy(), Dp.numpy(), device=local_rank, stream=stream.cuda_stream)
-        r2 = pkg.qap_rlt2_bound(h2, T)
-        pkg.qap_destroy(h2)
+        pkg.qap_rlt2_load(h, Fp.numpy(), Dp.numpy())
+        r2 = pkg.qap_rlt2_bound(h, T)
     e3.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3)
@@ -258,6 +259,24 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
     assert r2["lb"] == lb, "e2e run must reproduce the device-resident bound bit for bit"
+
+    # B&B nodes/s (BASELINE config 2: nug12-shaped full branch-and-bound on one GPU)
+    bnb = None
+    if not args.no_bnb:
+        bi = qapgen.nug(12, SEED)
+        hb = pkg.qap_rlt2_create(12, bi.F, bi.D, device=local_rank, stream=stream.cuda_stream)
+        pkg.qap_bnb_solve(hb, BNB_ITERS)                     # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rb = pkg.qap_bnb_solve(hb, BNB_ITERS)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        pkg.qap_destroy(hb)
+        bnb = {"config": f"nug12-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node, UB0=inf, "
+                         "branch on lowest free facility, leaves n'<=3 enumerated",
+               "nodes_per_s": rb["bounded"] / dt, "bounded_nodes": rb["bounded"], "leaves": rb["leaves"],
+               "pruned": rb["pruned"], "opt": rb["opt"], "seconds": dt, "timer": "host wall clock"}
+    pkg.qap_destroy(h)
 
     if rank != 0:
         if dist:
@@ -294,7 +313,9 @@ def main():
             "roofline": roof,
             "e2e": {"value": T * e2e_steps * world / (ms_e2e / 1e3), "unit": "iters/s",
                     "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 80,
-                    "path": "qap_rlt2_create(host F,D) + qap_rlt2_bound(T) + qap_destroy per step"},
+                    "path": "per step: qap_rlt2_load(pinned host F, D) + qap_rlt2_bound(T=20) "
+                            "(result read back to the host)"},
+            "bnb": bnb,
             "gpu_launches": launches,
             "clocks": clk.summary()}
     if world == 1 and not args.no_cpu_baseline:

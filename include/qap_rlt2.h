@@ -87,6 +87,14 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D,
                            const qap_rlt2_opts *opts, qap_rlt2 **out);
 
 /*
+ * qap_rlt2_load — replace the instance of an existing handle by a new one of the same N
+ *   (HOST F, D copied host->device), then re-initialise the root node as qap_rlt2_create
+ *   does.  Reuses the device allocation (a batch of instances of one size needs one
+ *   handle).  Errors as qap_rlt2_create; on error the handle keeps its previous instance.
+ */
+qap_status qap_rlt2_load(qap_rlt2 *h, const int64_t *F, const int64_t *D);
+
+/*
  * qap_rlt2_fix — set the node's partial assignment Φ = {(fac[t], loc[t]) : t < m}
  *   (facility fac[t] at location loc[t]; HOST arrays of length m; m = 0 is the root).
  *   REPLACES any previous Φ.  Rebuilds the reduced problem of the n = N-m free

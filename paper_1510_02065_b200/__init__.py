@@ -28,7 +28,7 @@ QAP_FLAG_OVERLAP = 2
 PHASE_ITER0, PHASE_TRANSFER, PHASE_CONC_D, PHASE_CONC_C, PHASE_CONC_B = range(5)
 KERNEL_KINDS = ["init", "sigma", "transfer", "lap2", "lap1", "lap0"]
 
-EXPORTS = ["qap_rlt2_create", "qap_rlt2_fix", "qap_rlt2_bound", "qap_rlt2_dual_sizes",
+EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound", "qap_rlt2_dual_sizes",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
            "qap_destroy", "qap_lap_batch", "qap_bnb_solve"]
 
@@ -65,6 +65,7 @@ def load_library(path: str = LIB_PATH):
     vp, i32, i64, f64 = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_double
     L.qap_rlt2_create.argtypes = [i32, vp, vp, ct.POINTER(_Opts), ct.POINTER(vp)]
     L.qap_rlt2_fix.argtypes = [vp, i32, vp, vp]
+    L.qap_rlt2_load.argtypes = [vp, vp, vp]
     L.qap_rlt2_bound.argtypes = [vp, i32, f64, f64, ct.POINTER(_Result)]
     L.qap_rlt2_dual_sizes.argtypes = [vp, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
     L.qap_rlt2_dual_copy.argtypes = [vp, vp, vp, vp, ct.POINTER(f64)]
@@ -136,6 +137,15 @@ def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0,
     st = L.qap_rlt2_create(N, F.ctypes.data, D.ctypes.data, ct.byref(opts), ct.byref(out))
     _check(st, None)
     return Handle(out.value, N)
+
+
+def qap_rlt2_load(h: Handle, F, D) -> None:
+    """Replace the handle's instance (same N) from host arrays; resets to the root node."""
+    F = np.ascontiguousarray(F, dtype=np.int64)
+    D = np.ascontiguousarray(D, dtype=np.int64)
+    if F.shape != (h.N, h.N) or D.shape != (h.N, h.N):
+        raise ValueError("F and D must be N×N")
+    _check(load_library().qap_rlt2_load(h.ptr, F.ctypes.data, D.ctypes.data), h)
 
 
 def qap_rlt2_fix(h: Handle, fixed=()) -> None:

@@ -141,6 +141,21 @@ static void free_all(qap_rlt2 *h)
     for (auto e : h->pool) cudaEventDestroy(e);
 }
 
+static qap_status check_instance(qap_rlt2 *h, int N, const int64_t *F, const int64_t *D)
+{
+    if (!F || !D) return fail(h, QAP_E_ARG, "F or D is NULL");
+    int64_t maxf = 0, maxd = 0;
+    for (int64_t t = 0; t < (int64_t)N * N; t++) {
+        if (F[t] < 0 || D[t] < 0) return fail(h, QAP_E_ARG, "negative flow or distance entry");
+        maxf = F[t] > maxf ? F[t] : maxf;
+        maxd = D[t] > maxd ? D[t] : maxd;
+    }
+    // exactness of integer costs in fp64 (SPEC S:28): N^2 maxF maxD < 2^53
+    const long double bound = (long double)N * N * (long double)maxf * (long double)maxd;
+    if (bound >= 9007199254740992.0L) return fail(h, QAP_E_ARG, "N^2*maxF*maxD >= 2^53");
+    return QAP_OK;
+}
+
 extern "C" {
 
 qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
@@ -149,16 +164,10 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
     if (!out) return fail(nullptr, QAP_E_ARG, "out is NULL");
     *out = nullptr;
     if (N < 3 || N > kMaxN) return fail(nullptr, QAP_E_ARG, "N must be in [3, 64]");
-    if (!F || !D) return fail(nullptr, QAP_E_ARG, "F or D is NULL");
-    int64_t maxf = 0, maxd = 0;
-    for (int64_t t = 0; t < (int64_t)N * N; t++) {
-        if (F[t] < 0 || D[t] < 0) return fail(nullptr, QAP_E_ARG, "negative flow or distance entry");
-        maxf = F[t] > maxf ? F[t] : maxf;
-        maxd = D[t] > maxd ? D[t] : maxd;
+    {
+        qap_status st0 = check_instance(nullptr, N, F, D);
+        if (st0 != QAP_OK) return st0;
     }
-    // exactness of integer costs in fp64 (SPEC S:28): N^2 maxF maxD < 2^53
-    const long double bound = (long double)N * N * (long double)maxf * (long double)maxd;
-    if (bound >= 9007199254740992.0L) return fail(nullptr, QAP_E_ARG, "N^2*maxF*maxD >= 2^53");
 
     qap_rlt2 *h = new qap_rlt2();
     h->N = N;
@@ -243,6 +252,21 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
     }
     *out = h;
     return QAP_OK;
+}
+
+qap_status qap_rlt2_load(qap_rlt2 *h, const int64_t *F, const int64_t *D)
+{
+    if (!h) return QAP_E_ARG;
+    const int N = h->N;
+    qap_status st = check_instance(h, N, F, D);
+    if (st != QAP_OK) return st;
+    h->F.assign(F, F + (size_t)N * N);
+    h->Dist.assign(D, D + (size_t)N * N);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(h->dF, F, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h->dDist, D, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess)
+        return cuda_fail(h, e, "upload");
+    return qap_rlt2_fix(h, 0, nullptr, nullptr);
 }
 
 qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_t *loc)

@@ -175,7 +175,7 @@ __device__ __forceinline__ T sel_t(const T (&a)[CPL], int t)
 
 // Solve the m×m LAP whose row-major costs start at Mlane - lane (shared memory).
 // Outputs per owned column: poff (matched row × 8m bytes), v, ucol.
-template <int CPL>
+template <int CPL, bool COUNT>
 __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int lane, int (&poff)[CPL],
                                                double (&v)[CPL], double (&ucol)[CPL], int &steps)
 {
@@ -231,7 +231,7 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
                     minv[t] = __hiloint2double(0x7ff80000, __double2loint(minv[t]));
                 }
             }
-            steps++;
+            if (COUNT) steps++;
             if (j1free) {
                 jfree = j1;
                 break;
@@ -284,10 +284,13 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
 
 // Residual (reading R8), written IN PLACE over the smem cost block, + primal value S
 // (reading R9).  Returns S (all lanes) and sets `bad` if some residual fell below -tau.
-// p[t] receives the matched row of each owned column.
+// p[t] receives the matched row of each owned column.  One pass: the clamp to +0 is
+// applied directly; since tau >= 1e-9, the exact tau test (which needs max|M|) is only
+// evaluated when some raw residual is below -1e-9, from the original block `Mg` (global
+// memory, not yet overwritten — the residual is stored back after this returns).
 template <int CPL>
-__device__ __forceinline__ double warp_lap_epilogue(double *M, int m, int lane, const int (&poff)[CPL],
-                                                    int (&p)[CPL], const double (&v)[CPL],
+__device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg, int m, int lane,
+                                                    const int (&poff)[CPL], int (&p)[CPL], const double (&v)[CPL],
                                                     const double (&ucol)[CPL], double *urow, double *sel, bool &bad)
 {
     const int rowb = m * 8;
@@ -301,30 +304,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, int m, int lane, 
         }
     }
     __syncwarp();
-    // A negative raw residual is rare (rounding only): then the exact tau test runs on a
-    // recomputation below, before the block is overwritten.
-    bool neg = false;
-#pragma unroll
-    for (int t = 0; t < CPL; t++) {
-        const int c = lane + 32 * t;
-        if (c < m) {
-            const double vc = v[t];
-#pragma unroll 4
-            for (int r = 0; r < m; r++) neg |= ((M[r * m + c] - urow[r]) - vc) < 0.0;
-        }
-    }
-    double mn = 0.0, mx = 0.0;
-    if (__any_sync(FULL_MASK, neg)) {
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            const int c = lane + 32 * t;
-            if (c < m)
-                for (int r = 0; r < m; r++) {
-                    mx = fmax(mx, fabs(M[r * m + c]));
-                    mn = fmin(mn, (M[r * m + c] - urow[r]) - v[t]);
-                }
-        }
-    }
+    double mn = 0.0;
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         const int c = lane + 32 * t;
@@ -335,6 +315,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, int m, int lane, 
 #pragma unroll 4
             for (int r = 0; r < m; r++) {
                 const double x = (Mc[r * m] - urow[r]) - vc;
+                mn = x < mn ? x : mn;
                 Mc[r * m] = (x > 0.0 && pr != r) ? x : 0.0;  // x <= 0 (incl. -0) or assigned -> +0
             }
         }
@@ -343,13 +324,22 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, int m, int lane, 
     if (lane == 0)
         for (int r = 0; r < m; r++) S = S + sel[r];  // sequential row order (reading R9)
     S = __shfl_sync(FULL_MASK, S, 0);
+    bad = false;
+    if (__any_sync(FULL_MASK, mn < -1e-9)) {  // rare: exact test tau = 1e-9 max(1, max|M|)
+        double mx = 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, o));
-        mn = fmin(mn, __shfl_xor_sync(FULL_MASK, mn, o));
+        for (int t = 0; t < CPL; t++) {
+            const int c = lane + 32 * t;
+            if (c < m)
+                for (int r = 0; r < m; r++) mx = fmax(mx, fabs(Mg[r * m + c]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(FULL_MASK, mx, o));
+            mn = fmin(mn, __shfl_xor_sync(FULL_MASK, mn, o));
+        }
+        bad = mn < -1e-9 * fmax(1.0, mx);
     }
-    const double tau = 1e-9 * fmax(1.0, mx);
-    bad = mn < -tau;
     fence_proxy_async();  // residual (generic-proxy writes) -> visible to the TMA store
     __syncwarp();
     return S;
@@ -476,9 +466,10 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         int poff[CPL], p[CPL];
         double v[CPL], ucol[CPL];
         int steps = 0;
-        warp_lap_solve<CPL>(M + lane, m, lane, poff, v, ucol, steps);
+        if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M + lane, m, lane, poff, v, ucol, steps);
+        else warp_lap_solve<CPL, false>(M + lane, m, lane, poff, v, ucol, steps);
         bool bad;
-        const double S = warp_lap_epilogue<CPL>(M, m, lane, poff, p, v, ucol, urow, sel, bad);
+        const double S = warp_lap_epilogue<CPL>(M, a.src + b * a.ld, m, lane, poff, p, v, ucol, urow, sel, bad);
         anybad |= bad;
         if (lane == 0) {
             tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global

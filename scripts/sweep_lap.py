@@ -8,7 +8,7 @@ import qapgen
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 # (flags, lap_cfg)
-cfgs = [(0, 0x20), (0, 0x1c), (pkg.QAP_FLAG_OVERLAP, 0x10), (pkg.QAP_FLAG_OVERLAP, 0x0c)]
+cfgs = [(0, 0x20), (0, 0x1c)]
 torch.cuda.set_device(0)
 inst = qapgen.nug(n, 1)
 ref = None
