@@ -185,6 +185,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lap-warps", type=int, default=0)
     ap.add_argument("--no-bnb", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded bound")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -207,8 +208,31 @@ def main():
     n, T = args.n, T_ITERS
     inst = qapgen.nug(n, SEED)
     stream = torch.cuda.current_stream()
-    h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
-                            flags=pkg.QAP_FLAG_TIME_KERNELS, lap_warps=args.lap_warps)
+    sharded, shard_err = False, None
+    if world > 1 and not args.replicas:
+        # one bound sharded over all ranks: NCCL id from rank 0
+        try:
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(pkg.qap_nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
+                                    flags=pkg.QAP_FLAG_TIME_KERNELS, lap_warps=args.lap_warps,
+                                    world=world, rank=rank, nccl_id=bytes(uid.cpu().numpy()))
+            sharded = True
+        except Exception as ex:  # reported in the JSON line; replicas below
+            shard_err = f"{type(ex).__name__}: {ex}"
+    if not sharded:
+        h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
+                                flags=pkg.QAP_FLAG_TIME_KERNELS, lap_warps=args.lap_warps)
+    if dist:
+        ok = torch.tensor([1 if sharded else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if sharded and ok.item() == 0:  # some rank failed: everybody falls back to replicas
+            pkg.qap_destroy(h)
+            sharded = False
+            h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
+                                    flags=pkg.QAP_FLAG_TIME_KERNELS, lap_warps=args.lap_warps)
 
     def step():
         pkg.qap_rlt2_fix(h, ())
@@ -236,6 +260,10 @@ def main():
         ms = float(t.item())
     ks = pkg.qap_rlt2_kernel_stats(h, reset=True)
     lb = r["lb"]
+    shard_entries = None
+    if sharded:
+        si = pkg.qap_rlt2_shard_info(h)
+        shard_entries = (si["blk_hi"] - si["blk_lo"]) * (n - 2) ** 2
 
     # e2e through the public API with HOST buffers: every step copies the instance (F, D)
     # from pinned host memory into the handle (qap_rlt2_load = H2D + root init), runs the
@@ -262,7 +290,7 @@ def main():
 
     # B&B nodes/s (BASELINE config 2: nug12-shaped full branch-and-bound on one GPU)
     bnb = None
-    if not args.no_bnb:
+    if not args.no_bnb and rank == 0:
         bi = qapgen.nug(12, SEED)
         hb = pkg.qap_rlt2_create(12, bi.F, bi.D, device=local_rank, stream=stream.cuda_stream)
         pkg.qap_bnb_solve(hb, BNB_ITERS)                     # warm-up
@@ -283,7 +311,8 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    iters_total = T * args.steps * world
+    units = 1 if sharded else world  # one sharded bound, or one bound per rank
+    iters_total = T * args.steps * units
     value = iters_total / (ms / 1e3)
     peak, peak_src = measured_peaks()
     per = {}
@@ -292,6 +321,8 @@ def main():
             per[k] = {"launches": v["launches"], "avg_ms": v["ms"] / v["launches"],
                       "share": v["ms"] / max(1e-9, sum(x["ms"] for x in ks.values()))}
     alg_bytes = 16 * n_stored(n)       # one read + one write of every stored D entry
+    if sharded:                        # this rank's share of the stored blocks
+        alg_bytes = 16 * shard_entries
     dom = max(("lap2", "transfer"), key=lambda k: per.get(k, {}).get("share", 0))
     achieved = alg_bytes / (per[dom]["avg_ms"] / 1e3) / 1e9
     roof = {"bound": "hbm", "kernel": {"lap2": "k_lap<1> (level-2 concentration)",
@@ -302,16 +333,19 @@ def main():
                + per["lap1"]["avg_ms"] * T / (T + 1) + per["lap0"]["avg_ms"])
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_cfg(n, {"parallelism": "replicas (one independent bound per GPU)" if world > 1
-                                       else "1 GPU"}),
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_cfg(n, {"parallelism": (f"one bound sharded over {world} GPUs (first-facility LPT "
+                                                       "partition, NCCL exchange + all-gather)") if sharded else
+                                       ("replicas (one independent bound per GPU)" + (f"; sharding failed: {shard_err}"
+                                        if shard_err else "")) if world > 1 else "1 GPU"}),
             "laps_per_s": value * laps_per_iter(n),
             "lb": lb,
-            "effective_hbm": {"GB_per_s": alg_bytes * iters_total / world / (ms / 1e3) / 1e9,
-                              "frac": alg_bytes * iters_total / world / (ms / 1e3) / 1e9 / peak},
+            "effective_hbm": {"GB_per_s": alg_bytes * T * args.steps / (ms / 1e3) / 1e9,
+                              "frac": alg_bytes * T * args.steps / (ms / 1e3) / 1e9 / peak,
+                              "note": "per GPU"},
             "kernels": per, "iter_kernel_ms": iter_ms,
             "roofline": roof,
-            "e2e": {"value": T * e2e_steps * world / (ms_e2e / 1e3), "unit": "iters/s",
+            "e2e": {"value": T * e2e_steps * units / (ms_e2e / 1e3), "unit": "iters/s",
                     "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 80,
                     "path": "per step: qap_rlt2_load(pinned host F, D) + qap_rlt2_bound(T=20) "
                             "(result read back to the host)"},

@@ -56,7 +56,11 @@ typedef struct {
     int32_t device;       /* CUDA device ordinal; -1 = current device                         */
     void *cuda_stream;    /* cudaStream_t to enqueue on; NULL = legacy default stream          */
     int32_t flags;        /* QAP_FLAG_* bit set                                                */
-    int32_t lap_warps;    /* warps per CTA of the level-2 LAP kernel; 0 = default              */
+    int32_t lap_warps;    /* level-2 LAP launch config: warps per CTA (bits 0-7); 0 = default  */
+    int32_t world;        /* ranks sharing ONE bound (<= 1: single GPU)         */
+    int32_t rank;         /* this process's rank in [0, world)                                 */
+    const void *nccl_id;  /* world > 1: 128-byte ncclUniqueId from qap_nccl_unique_id on rank
+                             0, broadcast by the caller; every rank then calls create (collective) */
 } qap_rlt2_opts;
 
 #define QAP_FLAG_TIME_KERNELS 1   /* record CUDA events around every launch (qap_rlt2_kernel_stats) */
@@ -162,6 +166,34 @@ qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase);
 #define QAP_K_LAP0 5
 #define QAP_K_COUNT 6
 qap_status qap_rlt2_kernel_stats(qap_rlt2 *h, int64_t *launches, double *ms, int32_t reset);
+
+/*
+ * Multi-GPU sharding of one bound.  With opts->world = G > 1
+ * the stored blocks are partitioned by first facility into G contiguous ranges balanced
+ * by block count; every rank holds only its range.  Per iteration: the partials of the
+ * complementary classes whose members straddle two ranks are exchanged (grouped NCCL
+ * send/recv = all-to-all), the level-2 values S are all-gathered (NCCL broadcasts), and
+ * the level-1/level-0 concentrations run replicated, so LB bits are identical on every
+ * rank and equal to the single-GPU bits.  All calls on a sharded handle are collective.
+ * qap_rlt2_dual_copy on a sharded handle writes only this rank's blocks of D.
+ */
+qap_status qap_nccl_unique_id(void *id128);   /* rank 0; 128 bytes, broadcast by the caller */
+/* Shard geometry of h at the current node (any pointer may be NULL).                 */
+qap_status qap_rlt2_shard_info(const qap_rlt2 *h, int32_t *world, int32_t *rank, int64_t *blk_lo,
+                               int64_t *blk_hi, int64_t *tiles_local, int64_t *tiles_shared,
+                               int64_t *slots);
+/* Host-only: the shard plan of `rank` among `world` for size n (no GPU needed): block
+ * ranges blk_lo[world+1], exchanged tiles per peer peer_slots[world], this rank's tile list
+ * (global tile ids, kind | slot<<2) — used to test the partition logic.               */
+qap_status qap_shard_plan(int32_t n, int32_t world, int32_t rank, int64_t *blk_lo, int64_t *peer_slots,
+                          int32_t *tiles, int32_t *tinfo, int64_t tiles_cap, int64_t *n_tiles);
+/* In-process group of G shards (one process; the collectives become device copies) for
+ * single-GPU testing of the sharded path: out[G] handles; bound them with
+ * qap_rlt2_group_bound (out[G] results); fix each member with qap_rlt2_fix.           */
+qap_status qap_rlt2_create_group(int32_t G, int32_t N, const int64_t *F, const int64_t *D,
+                                 const qap_rlt2_opts *opts, qap_rlt2 **out);
+qap_status qap_rlt2_group_bound(qap_rlt2 *const *hs, int32_t G, int32_t max_iters, double K, double UB,
+                                qap_rlt2_result *out);
 
 /* Last error message of h (or of the last failed create when h == NULL).             */
 const char *qap_last_error(const qap_rlt2 *h);

@@ -30,7 +30,8 @@ KERNEL_KINDS = ["init", "sigma", "transfer", "lap2", "lap1", "lap0"]
 
 EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound", "qap_rlt2_dual_sizes",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
-           "qap_destroy", "qap_lap_batch", "qap_bnb_solve"]
+           "qap_destroy", "qap_lap_batch", "qap_bnb_solve", "qap_nccl_unique_id", "qap_rlt2_shard_info",
+           "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound"]
 
 
 class QapError(RuntimeError):
@@ -41,7 +42,8 @@ class QapError(RuntimeError):
 
 class _Opts(ct.Structure):
     _fields_ = [("device", ct.c_int32), ("cuda_stream", ct.c_void_p), ("flags", ct.c_int32),
-                ("lap_warps", ct.c_int32)]
+                ("lap_warps", ct.c_int32), ("world", ct.c_int32), ("rank", ct.c_int32),
+                ("nccl_id", ct.c_void_p)]
 
 
 class _Result(ct.Structure):
@@ -78,6 +80,11 @@ def load_library(path: str = LIB_PATH):
     L.qap_lap_batch.argtypes = [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, ct.POINTER(i64), vp, ct.POINTER(i64),
                                 ct.POINTER(i64), ct.POINTER(i64)]
+    L.qap_nccl_unique_id.argtypes = [vp]
+    L.qap_rlt2_shard_info.argtypes = [vp] + [vp] * 7
+    L.qap_shard_plan.argtypes = [i32, i32, i32, vp, vp, vp, vp, i64, ct.POINTER(i64)]
+    L.qap_rlt2_create_group.argtypes = [i32, i32, vp, vp, ct.POINTER(_Opts), vp]
+    L.qap_rlt2_group_bound.argtypes = [vp, i32, i32, f64, f64, vp]
     for name in EXPORTS:
         if name not in ("qap_last_error", "qap_destroy"):
             getattr(L, name).restype = ct.c_int
@@ -126,13 +133,18 @@ class Handle:
         self.close()
 
 
-def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0, lap_warps: int = 0) -> Handle:
+def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0, lap_warps: int = 0,
+                    world: int = 1, rank: int = 0, nccl_id: bytes | None = None) -> Handle:
+    """world > 1: this process's shard of one bound shared by `world` processes (collective;
+    nccl_id = qap_nccl_unique_id() from rank 0, broadcast by the caller)."""
     L = load_library()
     F = np.ascontiguousarray(F, dtype=np.int64)
     D = np.ascontiguousarray(D, dtype=np.int64)
     if F.shape != (N, N) or D.shape != (N, N):
         raise ValueError("F and D must be N×N")
-    opts = _Opts(device, stream if stream is not None else _current_stream(), flags, lap_warps)
+    idbuf = ct.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+    opts = _Opts(device, stream if stream is not None else _current_stream(), flags, lap_warps, world, rank,
+                 ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None)
     out = ct.c_void_p()
     st = L.qap_rlt2_create(N, F.ctypes.data, D.ctypes.data, ct.byref(opts), ct.byref(out))
     _check(st, None)
@@ -225,6 +237,87 @@ def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf) 
     _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, ct.byref(opt), perm.ctypes.data, ct.byref(b),
                                         ct.byref(l), ct.byref(p)), h)
     return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value)
+
+
+def qap_nccl_unique_id() -> bytes:
+    buf = ct.create_string_buffer(128)
+    _check(load_library().qap_nccl_unique_id(buf), None)
+    return buf.raw
+
+
+def qap_rlt2_shard_info(h: Handle) -> dict:
+    w, r = ct.c_int32(), ct.c_int32()
+    lo, hi, tl, ts, sl = (ct.c_int64() for _ in range(5))
+    _check(load_library().qap_rlt2_shard_info(h.ptr, ct.byref(w), ct.byref(r), ct.byref(lo), ct.byref(hi),
+                                              ct.byref(tl), ct.byref(ts), ct.byref(sl)), h)
+    return dict(world=w.value, rank=r.value, blk_lo=lo.value, blk_hi=hi.value, tiles_local=tl.value,
+                tiles_shared=ts.value, slots=sl.value)
+
+
+def qap_shard_plan(n: int, world: int, rank: int) -> dict:
+    """Host-only shard plan (no GPU): block ranges, per-peer exchanged tiles, tile list."""
+    L = load_library()
+    cnt = ct.c_int64()
+    blk = np.zeros(world + 1, np.int64)
+    peer = np.zeros(world, np.int64)
+    _check(L.qap_shard_plan(n, world, rank, blk.ctypes.data, peer.ctypes.data, None, None, 0, ct.byref(cnt)), None)
+    tiles = np.zeros(max(cnt.value, 1), np.int32)
+    tinfo = np.zeros(max(cnt.value, 1), np.int32)
+    _check(L.qap_shard_plan(n, world, rank, None, None, tiles.ctypes.data, tinfo.ctypes.data, cnt.value,
+                            ct.byref(cnt)), None)
+    return dict(blk_lo=blk, peer_slots=peer, tiles=tiles[:cnt.value], kind=tinfo[:cnt.value] & 3,
+                slot=tinfo[:cnt.value] >> 2)
+
+
+class Group:
+    """In-process group of G shards of one bound (single-GPU test vehicle of the sharded path)."""
+
+    def __init__(self, G: int, N: int, F, D, device: int = -1, flags: int = 0, lap_warps: int = 0):
+        L = load_library()
+        F = np.ascontiguousarray(F, dtype=np.int64)
+        D = np.ascontiguousarray(D, dtype=np.int64)
+        opts = _Opts(device, _current_stream(), flags, lap_warps, G, 0, None)
+        arr = (ct.c_void_p * G)()
+        _check(L.qap_rlt2_create_group(G, N, F.ctypes.data, D.ctypes.data, ct.byref(opts), arr), None)
+        self.G, self.N = G, N
+        self.handles = [Handle(arr[r], N) for r in range(G)]
+        self._arr = arr
+
+    def fix(self, fixed=()):
+        for h in self.handles:
+            qap_rlt2_fix(h, fixed)
+
+    def bound(self, max_iters: int, K: float = 0.0, UB: float = math.inf, trace: bool = False):
+        G = self.G
+        res = (_Result * G)()
+        bufs = []
+        for r in range(G):
+            if trace and max_iters > 0:
+                b = (ct.c_double * max_iters)()
+                bufs.append(b)
+                res[r].lb_trace = ct.cast(b, ct.POINTER(ct.c_double))
+                res[r].lb_trace_cap = max_iters
+        arr = (ct.c_void_p * G)(*[h.ptr for h in self.handles])
+        _check(load_library().qap_rlt2_group_bound(arr, G, max_iters, K, UB, res), self.handles[0])
+        out = []
+        for r in range(G):
+            d = dict(lb=res[r].lb, lb_glb=res[r].lb_glb, iters=res[r].iters, status=res[r].status)
+            if bufs:
+                d["trace"] = np.array(bufs[r][: res[r].iters])
+            out.append(d)
+        return out
+
+    def dual(self):
+        """B, C (replicated; from rank 0) and D assembled from every shard."""
+        B, C, D, lb = qap_rlt2_dual_copy(self.handles[0])
+        L = load_library()
+        for h in self.handles[1:]:
+            _check(L.qap_rlt2_dual_copy(h.ptr, None, None, D.ctypes.data, None), h)
+        return B, C, D, lb
+
+    def close(self):
+        for h in self.handles:
+            h.close()
 
 
 class RLT2Bound:

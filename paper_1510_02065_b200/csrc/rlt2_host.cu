@@ -14,6 +14,7 @@
 
 #include "../../include/qap_rlt2.h"
 #include "rlt2_internal.h"
+#include "rlt2_shard.h"
 
 using namespace rlt2;
 
@@ -55,6 +56,15 @@ struct qap_rlt2 {
     int64_t launches[QAP_K_COUNT] = {0};
     double ms[QAP_K_COUNT] = {0};
     int call_launches = 0;
+    // sharding of one bound over `world` ranks
+    int world = 1, rank = 0;
+    Transport *tp = nullptr;  // NCCL (one process per GPU); nullptr in an in-process group
+    bool loopback = false;    // member of an in-process group: the group driver moves data
+    ShardPlan plan;           // for the current n
+    int *dTiles = nullptr, *dTinfo = nullptr;
+    size_t tiles_cap = 0, slots_cap = 0;
+    int64_t dblk_cap = 0;     // stored blocks the D allocation can hold
+    double *dSend = nullptr, *dRecv = nullptr, *dSall = nullptr;
 };
 
 static std::string g_create_error;
@@ -134,6 +144,13 @@ static void free_all(qap_rlt2 *h)
     if (h->evJoin) cudaEventDestroy(h->evJoin);
     if (h->evS) cudaEventDestroy(h->evS);
     if (h->evL) cudaEventDestroy(h->evL);
+    cudaFree(h->dTiles);
+    cudaFree(h->dTinfo);
+    cudaFree(h->dSend);
+    cudaFree(h->dRecv);
+    cudaFree(h->dSall);
+    delete h->tp;
+    h->tp = nullptr;
     for (auto &t : h->pending) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
@@ -158,8 +175,17 @@ static qap_status check_instance(qap_rlt2 *h, int N, const int64_t *F, const int
 
 extern "C" {
 
+static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
+                              qap_rlt2 **out, bool loopback);
+
 qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
                            qap_rlt2 **out)
+{
+    return create_impl(N, F, D, opts, out, false);
+}
+
+static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
+                              qap_rlt2 **out, bool loopback)
 {
     if (!out) return fail(nullptr, QAP_E_ARG, "out is NULL");
     *out = nullptr;
@@ -169,8 +195,17 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
         if (st0 != QAP_OK) return st0;
     }
 
+    const int world = (opts && opts->world > 1) ? opts->world : 1;
+    const int rank = world > 1 ? opts->rank : 0;
+    if (world > 1) {
+        if (rank < 0 || rank >= world || world > 64) return fail(nullptr, QAP_E_ARG, "bad rank / world");
+        if (!loopback && !opts->nccl_id) return fail(nullptr, QAP_E_ARG, "world > 1 needs opts->nccl_id");
+    }
     qap_rlt2 *h = new qap_rlt2();
     h->N = N;
+    h->world = world;
+    h->rank = rank;
+    h->loopback = loopback;
     h->flags = opts ? opts->flags : 0;
     h->lap_warps = opts ? opts->lap_warps : 0;
     h->stream = opts ? static_cast<cudaStream_t>(opts->cuda_stream) : nullptr;
@@ -189,7 +224,21 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
 
     Geom gN;
     make_geom(N, gN);
-    const size_t bytesD = (size_t)gN.nblk * gN.ld2 * 8;
+    size_t bytesD = (size_t)gN.nblk * gN.ld2 * 8;
+    if (world > 1) {  // this rank's block slice, tile list and exchange slots: max over n <= N
+        ShardPlan P;
+        for (int n = 3; n <= N; n++) {
+            make_plan(n, world, rank, P);
+            Geom gn;
+            make_geom(n, gn);
+            const int64_t blk = P.blk_lo[rank + 1] - P.blk_lo[rank];
+            const int64_t cap = (blk * gn.ld2 + gN.ld2 - 1) / gN.ld2;  // in N-sized blocks
+            h->dblk_cap = h->dblk_cap > cap ? h->dblk_cap : cap;
+            h->tiles_cap = h->tiles_cap > P.tiles.size() ? h->tiles_cap : P.tiles.size();
+            h->slots_cap = h->slots_cap > (size_t)P.total_slots ? h->slots_cap : (size_t)P.total_slots;
+        }
+        bytesD = (size_t)(h->dblk_cap > 0 ? h->dblk_cap : 1) * gN.ld2 * 8;
+    }
     const size_t bytesC = (size_t)N * N * gN.ldc * 8;
     const size_t bytesB = (((size_t)N * N + 1) & ~size_t(1)) * 8;
     const size_t bytesS = (size_t)gN.nblk * 8;
@@ -223,6 +272,23 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
     ALLOC(h->dCtl, sizeof(Ctl));
     ALLOC(h->dTriples, (size_t)N * (N - 1) * (N - 2) / 6 * sizeof(int) + 16);
     ALLOC(h->dSched, sizeof(Sched));
+    if (world > 1) {
+        ALLOC(h->dTiles, h->tiles_cap * sizeof(int) + 16);
+        ALLOC(h->dTinfo, h->tiles_cap * sizeof(int) + 16);
+        ALLOC(h->dSend, h->slots_cap * kSlot * 8 + 16);
+        ALLOC(h->dRecv, h->slots_cap * kSlot * 8 + 16);
+        ALLOC(h->dSall, (size_t)gN.nblk * 8 + 16);
+        if (!loopback) {
+            const char *why = "";
+            h->tp = make_nccl_transport(opts->nccl_id, world, rank, h->device, &why);
+            if (!h->tp) {
+                std::string msg = std::string("NCCL transport: ") + why;
+                free_all(h);
+                delete h;
+                return fail(nullptr, QAP_E_NCCL, msg);
+            }
+        }
+    }
     {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -295,6 +361,24 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
         nd.fac[t] = fac[t];
         nd.loc[t] = loc[t];
     }
+    if (h->world > 1) {
+        make_plan(nd.n, h->world, h->rank, h->plan);
+        Geom gn;
+        make_geom(nd.n, gn);
+        Geom gN;
+        make_geom(N, gN);
+        const int64_t blk = h->plan.blk_lo[h->rank + 1] - h->plan.blk_lo[h->rank];
+        if (blk * gn.ld2 > h->dblk_cap * gN.ld2 || h->plan.tiles.size() > h->tiles_cap ||
+            (size_t)h->plan.total_slots > h->slots_cap)
+            return fail(h, QAP_E_CAPACITY, "shard buffers too small for this node");
+        cudaError_t e0;
+        if (!h->plan.tiles.empty() &&
+            ((e0 = cudaMemcpy(h->dTiles, h->plan.tiles.data(), h->plan.tiles.size() * sizeof(int),
+                              cudaMemcpyHostToDevice)) != cudaSuccess ||
+             (e0 = cudaMemcpy(h->dTinfo, h->plan.tinfo.data(), h->plan.tinfo.size() * sizeof(int),
+                              cudaMemcpyHostToDevice)) != cudaSuccess))
+            return cuda_fail(h, e0, "tile lists");
+    }
     h->node = nd;
     make_geom(nd.n, h->geom);
     h->call_launches = 0;
@@ -314,10 +398,81 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
 // LAP kernel (CONC_D) on the high-priority stream sL concurrently with it: LAP warps take
 // blocks in facility order and wait for the transfer of their facility on the device
 // (Sched counters).  Both join back into `st`.
+static TransferArgs transfer_args(qap_rlt2 *h, int publish)
+{
+    TransferArgs A{};
+    A.g = h->geom;
+    A.D = h->dD;
+    A.sigma = h->dSigma;
+    A.triples = h->dTriples;
+    A.d_zero = h->d_zero;
+    A.ctl = h->dCtl;
+    A.sched = h->dSched;
+    A.ntile = (h->geom.n + TT - 1) / TT;
+    A.publish = publish;
+    if (h->world > 1) {
+        A.tiles = h->dTiles;
+        A.tinfo = h->dTinfo;
+        for (int f = 0; f < h->geom.n; f++) A.loc_off[f] = h->plan.loc_off[f];
+        A.sendbuf = h->dSend;
+        A.recvbuf = h->dRecv;
+    }
+    return A;
+}
+
+// Sharded iteration, one sub-phase (sub = 0 before the collective, 1 after it):
+//   TRANSFER: 0 = sigma + pack the partials of shared tiles, 1 = apply (class means)
+//   CONC_D:   0 = level-2 LAPs of the local blocks (S -> S_all slice), 1 = credit all S to C
+static cudaError_t run_shard_sub(qap_rlt2 *h, int phase, int sub, cudaStream_t st)
+{
+    cudaError_t e = cudaSuccess;
+    const Geom &g = h->geom;
+    const ShardPlan &P = h->plan;
+    if (phase == QAP_PHASE_TRANSFER && sub == 0) {
+        e = launch(h, QAP_K_SIGMA, st, [&](cudaStream_t s) {
+            return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->dSched, s);
+        });
+        if (e) return e;
+        TransferArgs A = transfer_args(h, 0);
+        A.pack = 1;
+        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, (int)P.tiles.size(), s); });
+    } else if (phase == QAP_PHASE_TRANSFER && sub == 1) {
+        TransferArgs A = transfer_args(h, 0);
+        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, (int)P.tiles.size(), s); });
+        h->d_zero = 0;
+        h->b_zero = h->c_zero = 1;
+    } else if (phase == QAP_PHASE_CONC_D && sub == 0) {
+        const int64_t cnt = P.blk_lo[h->rank + 1] - P.blk_lo[h->rank];
+        e = launch(h, QAP_K_LAP2, st, [&](cudaStream_t s) {
+            return launch_lap_l2_local(g, h->dD, cnt, h->dSall + P.blk_lo[h->rank], h->dCtl, h->num_sms,
+                                       h->lap_warps, h->dSched, s);  // S rank-major
+        });
+    } else if (phase == QAP_PHASE_CONC_D && sub == 1) {
+        Offsets pos{};
+        for (int f = 0; f < g.n; f++) pos.off[f] = P.pos_off[f];
+        e = launch(h, QAP_K_LAP2, st, [&](cudaStream_t s) { return launch_credit(g, h->dSall, pos, h->dC, h->dCtl, s); });
+        h->c_zero = 0;
+    }
+    return e;
+}
+
 static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused)
 {
     cudaError_t e = cudaSuccess;
     const Geom &g = h->geom;
+    if (h->world > 1 && (phase == QAP_PHASE_TRANSFER || phase == QAP_PHASE_CONC_D)) {
+        // NCCL mode: sub-phase, collective, sub-phase (an in-process group calls the
+        // sub-phases itself, see qap_rlt2_group_bound)
+        const int p0 = phase, p1 = fused ? QAP_PHASE_CONC_D : phase;
+        for (int ph = p0; ph <= p1; ph++) {
+            if ((e = run_shard_sub(h, ph, 0, st)) != cudaSuccess) return e;
+            e = ph == QAP_PHASE_TRANSFER ? h->tp->exchange(h->plan, h->dSend, h->dRecv, st)
+                                         : h->tp->allgather(h->plan, h->dSall, st);
+            if (e != cudaSuccess) return e;
+            if ((e = run_shard_sub(h, ph, 1, st)) != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     switch (phase) {
     case QAP_PHASE_ITER0:
         e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
@@ -347,9 +502,8 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
                 if ((e = cudaEventRecord(h->evS, sT)) != cudaSuccess) return e;
                 if ((e = cudaStreamWaitEvent(sL, h->evS, 0)) != cudaSuccess) return e;
             }
-            e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {
-                return launch_transfer(g, h->dD, h->dSigma, h->dTriples, h->d_zero, h->dCtl, h->dSched, ov ? 1 : 0, s);
-            });
+            const TransferArgs A = transfer_args(h, ov ? 1 : 0);
+            e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) { return launch_transfer(A, 0, s); });
             if (e) return e;
             h->d_zero = 0;
             h->b_zero = h->c_zero = 1;
@@ -402,6 +556,7 @@ static qap_status read_ctl(qap_rlt2 *h, Ctl &c)
 qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase)
 {
     if (!h) return QAP_E_ARG;
+    if (h->world > 1) return fail(h, QAP_E_STATE, "qap_rlt2_step is single-rank only");
     const int expect = h->next_phase == PH_FRESH ? QAP_PHASE_ITER0 : h->next_phase;
     if (phase != expect) return fail(h, QAP_E_STATE, "phases must run in Algorithm-1 order");
     h->call_launches = 0;
@@ -420,6 +575,7 @@ qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, q
     if (h->next_phase != PH_FRESH && h->next_phase != QAP_PHASE_TRANSFER)
         return fail(h, QAP_E_STATE, "bound called in the middle of an iteration");
     if (max_iters > h->trace_cap) return fail(h, QAP_E_ARG, "max_iters above the trace capacity (4096)");
+    if (h->loopback) return fail(h, QAP_E_STATE, "in-process group member: use qap_rlt2_group_bound");
     h->call_launches = 0;
     cudaError_t e = launch_ctl_begin(h->dCtl, K, UB, h->trace_cap, h->stream);
     h->call_launches++;
@@ -481,9 +637,19 @@ qap_status qap_rlt2_dual_copy(const qap_rlt2 *hc, double *B, double *C, double *
     }
     if (D) {
         const size_t w = (size_t)(n - 2) * (n - 2) * 8;
-        if (h->d_zero) memset(D, 0, w * g.nblk);
-        else if ((e = cudaMemcpy2D(D, w, h->dD, g.ld2 * 8, w, g.nblk, cudaMemcpyDeviceToHost)) != cudaSuccess)
-            return cuda_fail(h, e, "copy D");
+        // sharded: only this rank's blocks (at their global positions); the rest is untouched
+        for (int f = 0; f < (h->world > 1 ? n : 1); f++) {
+            if (h->world > 1 && h->plan.owner[f] != h->rank) continue;
+            const int64_t b0 = h->world > 1 ? g.off[f] : 0;
+            const int64_t nb = h->world > 1 ? (f + 1 < n ? g.off[f + 1] : g.nblk) - g.off[f] : g.nblk;
+            const int64_t l0 = h->world > 1 ? b0 + h->plan.loc_off[f] : 0;
+            if (nb <= 0) continue;
+            double *Dout = D + (size_t)b0 * (n - 2) * (n - 2);
+            if (h->d_zero) memset(Dout, 0, w * nb);
+            else if ((e = cudaMemcpy2D(Dout, w, h->dD + (size_t)l0 * g.ld2, g.ld2 * 8, w, nb,
+                                       cudaMemcpyDeviceToHost)) != cudaSuccess)
+                return cuda_fail(h, e, "copy D");
+        }
     }
     if (lb) {
         Ctl c;
@@ -642,4 +808,142 @@ qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int64
     return QAP_OK;
 }
 
+qap_status qap_nccl_unique_id(void *id128)
+{
+    if (!id128) return QAP_E_ARG;
+    const char *why = "";
+    if (nccl_unique_id(id128, &why) != 0) return fail(nullptr, QAP_E_NCCL, std::string("ncclGetUniqueId: ") + why);
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_shard_info(const qap_rlt2 *h, int32_t *world, int32_t *rank, int64_t *blk_lo, int64_t *blk_hi,
+                               int64_t *tiles_local, int64_t *tiles_shared, int64_t *slots)
+{
+    if (!h) return QAP_E_ARG;
+    if (world) *world = h->world;
+    if (rank) *rank = h->rank;
+    const bool sh = h->world > 1;
+    if (blk_lo) *blk_lo = sh ? h->plan.blk_lo[h->rank] : 0;
+    if (blk_hi) *blk_hi = sh ? h->plan.blk_lo[h->rank + 1] : h->geom.nblk;
+    if (tiles_local) *tiles_local = sh ? h->plan.n_local : -1;
+    if (tiles_shared) *tiles_shared = sh ? h->plan.n_agg + h->plan.n_hold : 0;
+    if (slots) *slots = sh ? h->plan.total_slots : 0;
+    return QAP_OK;
+}
+
+qap_status qap_shard_plan(int32_t n, int32_t world, int32_t rank, int64_t *blk_lo /*world+1*/, int64_t *peer_slots /*world*/,
+                          int32_t *tiles, int32_t *tinfo, int64_t tiles_cap, int64_t *n_tiles)
+{
+    if (n < 3 || n > kMaxN || world < 1 || world > 64 || rank < 0 || rank >= world) return QAP_E_ARG;
+    ShardPlan P;
+    make_plan(n, world, rank, P);
+    if (blk_lo)
+        for (int q = 0; q <= world; q++) blk_lo[q] = P.blk_lo[q];
+    if (peer_slots)
+        for (int q = 0; q < world; q++) peer_slots[q] = P.peer_slots[q];
+    if (n_tiles) *n_tiles = (int64_t)P.tiles.size();
+    if (tiles || tinfo) {
+        if ((int64_t)P.tiles.size() > tiles_cap) return QAP_E_ARG;
+        for (size_t t = 0; t < P.tiles.size(); t++) {
+            if (tiles) tiles[t] = P.tiles[t];
+            if (tinfo) tinfo[t] = P.tinfo[t];
+        }
+    }
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_create_group(int32_t G, int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
+                                 qap_rlt2 **out)
+{
+    if (!out || G < 1 || G > 64) return fail(nullptr, QAP_E_ARG, "bad group size");
+    for (int r = 0; r < G; r++) out[r] = nullptr;
+    qap_rlt2_opts o{};
+    if (opts) o = *opts;
+    else o.device = -1;
+    o.world = G;
+    o.nccl_id = nullptr;
+    for (int r = 0; r < G; r++) {
+        o.rank = r;
+        qap_status s = create_impl(N, F, D, &o, &out[r], G > 1);
+        if (s != QAP_OK) {
+            for (int q = 0; q < r; q++) qap_destroy(out[q]);
+            for (int q = 0; q < G; q++) out[q] = nullptr;
+            return s;
+        }
+    }
+    return QAP_OK;
+}
+
+// In-process group: every rank's phases in turn; the collectives are device copies.
+qap_status qap_rlt2_group_bound(qap_rlt2 *const *hs, int32_t G, int32_t max_iters, double K, double UB,
+                                qap_rlt2_result *out)
+{
+    if (!hs || !out || G < 1) return QAP_E_ARG;
+    if (G == 1) return qap_rlt2_bound(hs[0], max_iters, K, UB, out);
+    for (int r = 0; r < G; r++)
+        if (!hs[r] || hs[r]->world != G || hs[r]->rank != r || !hs[r]->loopback) return QAP_E_ARG;
+    qap_rlt2 *h0 = hs[0];
+    if (max_iters < 0 || !(K >= 0.0) || std::isnan(UB)) return fail(h0, QAP_E_ARG, "bad max_iters/K/UB");
+    cudaError_t e = cudaSuccess;
+#define GCHK(x)                                              \
+    if ((e = (x)) != cudaSuccess) return cuda_fail(h0, e, #x);
+    for (int r = 0; r < G; r++) {
+        qap_rlt2 *h = hs[r];
+        h->call_launches = 0;
+        GCHK(launch_ctl_begin(h->dCtl, K, UB, h->trace_cap, h->stream));
+        if (h->next_phase == PH_FRESH) {
+            GCHK(run_phase(h, QAP_PHASE_ITER0, h->stream, true));
+            h->next_phase = QAP_PHASE_TRANSFER;
+        }
+    }
+    for (int t = 0; t < max_iters; t++) {
+        for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_D; ph++) {
+            for (int r = 0; r < G; r++) GCHK(run_shard_sub(hs[r], ph, 0, hs[r]->stream));
+            GCHK(cudaDeviceSynchronize());
+            for (int r = 0; r < G; r++) {
+                const ShardPlan &P = hs[r]->plan;
+                for (int q = 0; q < G; q++) {
+                    if (q == r) continue;
+                    if (ph == QAP_PHASE_TRANSFER) {  // r receives q's partials of their shared tiles
+                        const ShardPlan &Q = hs[q]->plan;
+                        const size_t cnt = (size_t)P.peer_slots[q] * kSlot;
+                        if (cnt)
+                            GCHK(cudaMemcpy(hs[r]->dRecv + (size_t)P.peer_off[q] * kSlot,
+                                            hs[q]->dSend + (size_t)Q.peer_off[r] * kSlot, cnt * 8,
+                                            cudaMemcpyDeviceToDevice));
+                    } else {  // r receives q's level-2 values
+                        const size_t cnt = (size_t)(P.blk_lo[q + 1] - P.blk_lo[q]);
+                        if (cnt)
+                            GCHK(cudaMemcpy(hs[r]->dSall + P.blk_lo[q], hs[q]->dSall + P.blk_lo[q], cnt * 8,
+                                            cudaMemcpyDeviceToDevice));
+                    }
+                }
+            }
+            for (int r = 0; r < G; r++) GCHK(run_shard_sub(hs[r], ph, 1, hs[r]->stream));
+        }
+        for (int r = 0; r < G; r++) {
+            GCHK(run_phase(hs[r], QAP_PHASE_CONC_C, hs[r]->stream, true));
+            GCHK(run_phase(hs[r], QAP_PHASE_CONC_B, hs[r]->stream, true));
+        }
+    }
+#undef GCHK
+    for (int r = 0; r < G; r++) {
+        Ctl c;
+        qap_status s = read_ctl(hs[r], c);
+        if (s != QAP_OK) return s;
+        out[r].lb = c.lb;
+        out[r].lb_glb = c.lb_glb;
+        out[r].iters = c.iters;
+        out[r].status = c.status;
+        out[r].launches = hs[r]->call_launches;
+        if (out[r].lb_trace && out[r].lb_trace_cap > 0 && c.iters > 0) {
+            const int cnt = c.iters < out[r].lb_trace_cap ? c.iters : out[r].lb_trace_cap;
+            e = cudaMemcpy(out[r].lb_trace, hs[r]->dTrace, (size_t)cnt * 8, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) return cuda_fail(hs[r], e, "trace copy");
+        }
+    }
+    return QAP_OK;
+}
+
 }  // extern "C"
+

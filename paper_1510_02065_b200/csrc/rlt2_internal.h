@@ -78,14 +78,41 @@ cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const
 cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaStream_t st);
 cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double *sigma,
                          const Ctl *ctl, Sched *sched, cudaStream_t st);
-cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, const int *triples,
-                            int d_zero, const Ctl *ctl, Sched *sched, int publish, cudaStream_t st);
+constexpr int TT = 8;  // transfer tile edge (locations j, l, q)
+
+struct TransferArgs {
+    Geom g;
+    double *D;            // stored blocks of this rank (element dbase of the global layout first)
+    const double *sigma;  // all stored blocks
+    const int *triples;
+    int d_zero;
+    const Ctl *ctl;
+    Sched *sched;
+    int ntile;            // ceil(n / TT)
+    int publish;          // overlapped mode: publish per-facility progress
+    // sharded iteration (nullptr tiles: every tile, single rank)
+    const int *tiles;     // this rank's tiles (global tile id = triple * ntile^3 + tile)
+    const int *tinfo;     // kind | slot << 2 (slot: 512-double unit of the exchange buffers)
+    int64_t loc_off[kMaxN];  // local block index = global block id + loc_off[facility] (0: unsharded)
+    double *sendbuf;
+    const double *recvbuf;
+    int pack;             // 1: write this side's partial of AGG/HOLD tiles; 0: apply
+};
+cudaError_t launch_transfer(const TransferArgs &A, int ntiles_list, cudaStream_t st);
+struct Offsets {
+    int64_t off[kMaxN];
+};
+cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, double *C, const Ctl *ctl,
+                          cudaStream_t st);
 // Level-2 / level-1 / level-0 concentrations (one warp per LAP).
 // sched != nullptr (level 2 only): blocks come from the Sched queue in facility order and
 // wait for the transfer of their facility (concurrent-kernel overlap).
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B,
                              Ctl *ctl, double *trace, int num_sms, int lap_warps, Sched *sched,
                              int wait, cudaStream_t st);
+// Level-2 LAPs of `count` local blocks (sharded): S of block b to Sout[b].
+cudaError_t launch_lap_l2_local(const Geom &g, double *Dloc, int64_t count, double *Sout, Ctl *ctl, int num_sms,
+                                int lap_cfg, Sched *sched, cudaStream_t st);
 cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M,
                              const LapBatchOut &o, int num_sms, cudaStream_t st);
 

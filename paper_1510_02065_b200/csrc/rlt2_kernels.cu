@@ -484,6 +484,10 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         if (lane == 0) {
             switch (a.lvl) {
             case LAP_L2: {  // credit S to both complementary coefficients (reading R12)
+                if (a.bo.S) {  // sharded: S is all-gathered and credited by k_credit
+                    a.bo.S[b] = S;
+                    break;
+                }
                 const Geom &g = a.g;
                 facility_of(g, b, icur);
                 const int n = g.n, n1 = n - 1;
@@ -662,29 +666,47 @@ __global__ void k_sigma(const Geom g, const double *__restrict__ B, const double
 // doubles along its own contiguous index, transposed through shared memory, averaged,
 // and written back the same way — every stored entry is read once and written once.
 // ---------------------------------------------------------------------------------------
-constexpr int TT = 8;
 
 // Shared-memory index of element (x,y,z) of a tile view: rows padded to 9 doubles so
 // that the transposed reads of the mean phase are (nearly) bank-conflict free.
 __device__ __forceinline__ int tix(int x, int y, int z) { return x * (TT * (TT + 1)) + y * (TT + 1) + z; }
 constexpr unsigned NOIDX = 0xffffffffu;
 
-__global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__restrict__ D,
-                                                     const double *__restrict__ sigma, const int *__restrict__ triples,
-                                                     int d_zero, const Ctl *ctl, Sched *sched, int ntile, int publish)
+// Tile kinds of a sharded iteration.  A tile of facility triple (i,k,p) has
+// its views 0 and 1 (members e1, e2) on owner(i) and its view 2 (member e3) on owner(k).
+enum { TK_LOCAL = 0, TK_AGG = 1, TK_HOLD = 2 };
+
+template <bool SHARDED>
+__global__ void __launch_bounds__(256, 5) k_transfer(const TransferArgs A)
 {
-    if (ctl->stopped) return;
+    if (A.ctl->stopped) return;
     __shared__ double sv[3][TT * TT * (TT + 1)];  // the three member views of the tile's classes
     __shared__ unsigned rbase[3][TT * TT];        // element index of each view row in D (NOIDX: none)
     __shared__ double rsig[3][TT * TT];           // spread amount sigma of the row's block
-    const int n = g.n, m2 = n - 2;
+    const Geom &g = A.g;
+    const int n = g.n, m2 = n - 2, ntile = A.ntile;
     const int64_t ld2 = g.ld2;
-    const int tri = triples[blockIdx.y];  // (i,k,p), i<k<p, packed by k_init
+    int tq, tile, kind = TK_LOCAL, slot = 0;
+    if (SHARDED) {  // this rank's tile list
+        const int T = A.tiles[blockIdx.x];
+        const int nt3 = ntile * ntile * ntile;
+        tq = T / nt3;
+        tile = T - tq * nt3;
+        const int info = A.tinfo[blockIdx.x];
+        kind = info & 3;
+        slot = info >> 2;
+        if (A.pack && kind == TK_LOCAL) return;
+    } else {
+        tq = blockIdx.y;
+        tile = blockIdx.x;
+    }
+    const int tri = A.triples[tq];  // (i,k,p), i<k<p, packed by k_init
     const int i = tri & 0xff, k = (tri >> 8) & 0xff, p = tri >> 16;
-    const int tile = blockIdx.x;
     const int tl = tile / ntile, tj = tl / ntile;
     const int q0 = (tile - tl * ntile) * TT, l0 = (tl - tj * ntile) * TT, j0 = tj * TT;
     const int tid = threadIdx.x;
+    // which views live here
+    const bool has01 = kind != TK_HOLD, has2 = kind != TK_AGG;
 
     // rows: view 0 = D{ij,kl} row p-2 (rows (j,l)); view 1 = D{ij,pq} row k-1 (rows (j,q));
     //       view 2 = D{kl,pq} row i   (rows (l,q)).  sigma is fetched now, used after the
@@ -697,14 +719,14 @@ __global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__res
         else if (vw == 1) { r0 = j0 + x; r1 = q0 + y; }
         else { r0 = l0 + x; r1 = q0 + y; }
         unsigned base = NOIDX;
-        if (r0 < n && r1 < n && r0 != r1) {
+        if (r0 < n && r1 < n && r0 != r1 && (vw == 2 ? has2 : has01)) {
             int64_t bb;
             int row;
             if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; }
             else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; }
             else { bb = bid_of(g, k, r0, p, r1); row = i; }
-            base = (unsigned)(bb * ld2 + row * m2);
-            sg = sigma[bb];
+            sg = A.sigma[bb];
+            base = (unsigned)((bb + (SHARDED ? A.loc_off[vw == 2 ? k : i] : 0)) * ld2 + row * m2);
         }
         rbase[vw][tid & 63] = base;
     }
@@ -727,7 +749,7 @@ __global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__res
             unsigned ad = NOIDX;
             if (base != NOIDX && f < n && f != a && f != b) ad = base + (unsigned)(f - (f > a) - (f > b));
             addr[h][vw] = ad;
-            val[h][vw] = (ad != NOIDX && !d_zero) ? D[ad] : 0.0;
+            val[h][vw] = (ad != NOIDX && !A.d_zero) ? A.D[ad] : 0.0;
         }
     }
     if (tid < 3 * TT * TT) rsig[tid >> 6][tid & 63] = sg;
@@ -741,6 +763,8 @@ __global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__res
     }
     __syncthreads();
     // mean of each class (j,l,q): e1 = sv0[j][l][q], e2 = sv1[j][q][l], e3 = sv2[l][q][j]
+    // (reading R11: ((e1 + e2) + e3) / 3, the same operations on every rank)
+    const size_t xo = (size_t)slot * (TT * TT * TT);
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int e = tid + 256 * h;
@@ -748,12 +772,19 @@ __global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__res
         const int j = j0 + a, l = l0 + b, q = q0 + c;
         if (j < n && l < n && q < n && j != l && j != q && l != q) {
             const int e1 = tix(a, b, c), e2 = tix(a, c, b), e3 = tix(b, c, a);
-            const double mu = ((sv[0][e1] + sv[1][e2]) + sv[2][e3]) / 3.0;
-            sv[0][e1] = mu;
-            sv[1][e2] = mu;
-            sv[2][e3] = mu;
+            if (SHARDED && A.pack) {  // sharded, pass 1: this side's partial of the class
+                A.sendbuf[xo + e] = kind == TK_AGG ? sv[0][e1] + sv[1][e2] : sv[2][e3];
+            } else {
+                const double s12 = (SHARDED && kind == TK_HOLD) ? A.recvbuf[xo + e] : sv[0][e1] + sv[1][e2];
+                const double h3 = (SHARDED && kind == TK_AGG) ? A.recvbuf[xo + e] : sv[2][e3];
+                const double mu = (s12 + h3) / 3.0;
+                sv[0][e1] = mu;
+                sv[1][e2] = mu;
+                sv[2][e3] = mu;
+            }
         }
     }
+    if (SHARDED && A.pack) return;
     __syncthreads();
 #pragma unroll
     for (int h = 0; h < 2; h++) {
@@ -761,15 +792,32 @@ __global__ void __launch_bounds__(256, 5) k_transfer(const Geom g, double *__res
         const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
 #pragma unroll
         for (int vw = 0; vw < 3; vw++)
-            if (addr[h][vw] != NOIDX) D[addr[h][vw]] = sv[vw][tix(x, y, z)];
+            if (addr[h][vw] != NOIDX) A.D[addr[h][vw]] = sv[vw][tix(x, y, z)];
     }
-    if (publish) {  // overlapped mode: this tile of facility i is final (release)
+    if (A.publish) {  // overlapped mode: this tile of facility i is final (release)
         __threadfence();
         __syncthreads();
         if (tid == 0) {
             __threadfence();
-            atomicAdd(&sched->done[i], 1u);
+            atomicAdd(&A.sched->done[i], 1u);
         }
+    }
+}
+
+// Sharded iteration: level-2 values S of every stored block (all-gathered, global block
+// order) credited to both complementary coefficients (reading R12), on every rank.
+__global__ void k_credit(const Geom g, const double *__restrict__ S, const Offsets pos, double *__restrict__ C,
+                         const Ctl *ctl)
+{
+    if (ctl->stopped) return;
+    const int n = g.n, n1 = n - 1;
+    const int64_t n4 = (int64_t)n * n * n * n;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n4; x += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(x % n), k = (int)((x / n) % n), j = (int)((x / n / n) % n), i = (int)(x / n / n / n);
+        if (k <= i || l == j) continue;
+        const double v = S[bid_of(g, i, j, k, l) + pos.off[i]];
+        C[(int64_t)(i * n + j) * g.ldc + (k - 1) * n1 + (l - (l > j))] = v;
+        C[(int64_t)(k * n + l) * g.ldc + i * n1 + (j - (j > l))] = v;
     }
 }
 
@@ -802,14 +850,27 @@ cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double
     return cudaGetLastError();
 }
 
-cudaError_t launch_transfer(const Geom &g, double *D, const double *sigma, const int *triples, int d_zero,
-                            const Ctl *ctl, Sched *sched, int publish, cudaStream_t st)
+cudaError_t launch_transfer(const TransferArgs &A, int ntiles_list, cudaStream_t st)
 {
-    const int n = g.n;
-    const int ntile = (n + TT - 1) / TT;
-    const int ntri = n * (n - 1) * (n - 2) / 6;
-    dim3 grid(ntile * ntile * ntile, ntri);
-    k_transfer<<<grid, 256, 0, st>>>(g, D, sigma, triples, d_zero, ctl, sched, ntile, publish);
+    const int n = A.g.n;
+    if (A.tiles) {
+        if (ntiles_list <= 0) return cudaSuccess;
+        k_transfer<true><<<ntiles_list, 256, 0, st>>>(A);
+    } else {
+        const int ntri = n * (n - 1) * (n - 2) / 6;
+        dim3 grid(A.ntile * A.ntile * A.ntile, ntri);
+        k_transfer<false><<<grid, 256, 0, st>>>(A);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, double *C, const Ctl *ctl,
+                          cudaStream_t st)
+{
+    const int64_t tot = (int64_t)g.n * g.n * g.n * g.n;
+    int blocks = (int)((tot + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_credit<<<blocks, 256, 0, st>>>(g, S, pos, C, ctl);
     return cudaGetLastError();
 }
 
@@ -884,6 +945,25 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
     default: return cudaErrorInvalidValue;
     }
     return dispatch_lap(a, num_sms, wpc, st);
+}
+
+cudaError_t launch_lap_l2_local(const Geom &g, double *Dloc, int64_t count, double *Sout, Ctl *ctl, int num_sms,
+                                int lap_cfg, Sched *sched, cudaStream_t st)
+{
+    if (count <= 0) return cudaSuccess;
+    LapArgs a{};
+    a.lvl = LAP_L2;
+    a.g = g;
+    a.ctl = ctl;
+    a.m = g.n - 2;
+    a.count = count;
+    a.ld = g.ld2;
+    a.src = Dloc;
+    a.dst = Dloc;
+    a.bo.S = Sout;
+    a.sched = sched;  // dynamic queue (reset by k_sigma), no transfer waits
+    a.ntile3 = 0;
+    return dispatch_lap(a, num_sms, lap_cfg, st);
 }
 
 cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M, const LapBatchOut &o, int num_sms,
