@@ -286,3 +286,21 @@ def test_kernel_stats(torch, pkg):
     assert all(v["ms"] > 0 for k, v in s.items() if v["launches"])
     assert r["launches"] == 2 + 5 * 4 + 1    # ctl + iteration 0 (2) + 5 per iteration
     pkg.qap_destroy(h)
+
+
+def test_wide_columns_level2_n35(orc, torch, pkg):
+    """N = 35: the level-2 LAPs have m = 33 > 32 columns (2 columns per lane); one
+    iteration against the oracle (GLB exact, LB and sampled D within 1e-9)."""
+    inst = qapgen.taib(35, 1)
+    h = pkg.qap_rlt2_create(35, inst.F, inst.D)
+    g = pkg.qap_rlt2_bound(h, 1, trace=True)
+    st = orc.State(inst.F, inst.D)
+    o = st.bound(1, trace=True)
+    assert g["lb_glb"] == o["lb_glb"]
+    rel_close(g["trace"], o["trace"])
+    B, C, D, lb = gpu_state(pkg, h, 35)
+    rel_close(B, st.B)
+    rel_close(C, st.C)
+    idx = np.random.default_rng(1).integers(0, D.shape[0], 1500)
+    rel_close(D[idx], st.D[idx])
+    pkg.qap_destroy(h)

@@ -72,3 +72,10 @@ def test_group_n30_one_iteration(pkg):
     outs = grp.bound(1)
     assert all(o["lb"] == ref["lb"] for o in outs)
     grp.close()
+
+
+def test_nccl_loadable(pkg):
+    """The NCCL transport resolves libnccl (torch's copy) and creates a unique id."""
+    import torch.distributed  # noqa: F401  (torch's NCCL is loaded with torch)
+    uid = pkg.qap_nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
