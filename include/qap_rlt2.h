@@ -66,6 +66,7 @@ typedef struct {
 #define QAP_FLAG_TIME_KERNELS 1   /* record CUDA events around every launch (qap_rlt2_kernel_stats) */
 #define QAP_FLAG_OVERLAP 2        /* run the D transfer and the level-2 LAPs concurrently on two
                                      internal streams (experimental; default: one after the other) */
+#define QAP_FLAG_NO_GRAPH 4       /* do not replay the iteration loop from a cached CUDA graph     */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */

@@ -9,7 +9,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/qap_rlt2.h"
@@ -65,6 +67,9 @@ struct qap_rlt2 {
     size_t tiles_cap = 0, slots_cap = 0;
     int64_t dblk_cap = 0;     // stored blocks the D allocation can hold
     double *dSend = nullptr, *dRecv = nullptr, *dSall = nullptr;
+    // CUDA graphs of the iteration loop, keyed by (n, iterations, D still zero)
+    cudaStream_t sCap = nullptr;
+    std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
 };
 
 static std::string g_create_error;
@@ -144,6 +149,9 @@ static void free_all(qap_rlt2 *h)
     if (h->evJoin) cudaEventDestroy(h->evJoin);
     if (h->evS) cudaEventDestroy(h->evS);
     if (h->evL) cudaEventDestroy(h->evL);
+    for (auto &kv : h->graphs) cudaGraphExecDestroy(kv.second);
+    h->graphs.clear();
+    if (h->sCap) cudaStreamDestroy(h->sCap);
     cudaFree(h->dTiles);
     cudaFree(h->dTinfo);
     cudaFree(h->dSend);
@@ -296,7 +304,8 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
             (e = cudaStreamCreateWithPriority(&h->sT, cudaStreamNonBlocking, lo)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&h->evS, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&h->evL, cudaEventDisableTiming)) != cudaSuccess) {
+            (e = cudaEventCreateWithFlags(&h->evL, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&h->sCap, cudaStreamNonBlocking)) != cudaSuccess) {
             free_all(h);
             delete h;
             return cuda_fail(nullptr, e, "streams");
@@ -584,10 +593,44 @@ qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, q
         if ((e = run_phase(h, QAP_PHASE_ITER0, h->stream, true)) != cudaSuccess) return cuda_fail(h, e, "iteration 0");
         h->next_phase = QAP_PHASE_TRANSFER;
     }
-    for (int t = 0; t < max_iters; t++) {
-        for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_B; ph++) {
-            if (ph == QAP_PHASE_CONC_D) continue;  // enqueued together with TRANSFER
-            if ((e = run_phase(h, ph, h->stream, true)) != cudaSuccess) return cuda_fail(h, e, "iteration");
+    // The iteration loop is replayed from a CUDA graph (one launch instead of 5 per
+    // iteration: the B&B's small nodes are launch-bound), except when per-kernel event
+    // timing, the overlap mode or sharding is on.
+    const bool graphable = h->world == 1 && !(h->flags & (QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP | QAP_FLAG_NO_GRAPH));
+    if (graphable && max_iters > 0) {
+        const auto key = std::make_tuple(h->geom.n, max_iters, h->d_zero);
+        auto it = h->graphs.find(key);
+        if (it == h->graphs.end()) {
+            const int save_launches = h->call_launches, dz = h->d_zero;
+            cudaGraph_t graph = nullptr;
+            cudaGraphExec_t exec = nullptr;
+            if ((e = cudaStreamBeginCapture(h->sCap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+                return cuda_fail(h, e, "graph capture");
+            cudaError_t ec = cudaSuccess;
+            for (int t = 0; t < max_iters && ec == cudaSuccess; t++)
+                for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_B && ec == cudaSuccess; ph++)
+                    if (ph != QAP_PHASE_CONC_D) ec = run_phase(h, ph, h->sCap, true);
+            e = cudaStreamEndCapture(h->sCap, &graph);
+            if (ec != cudaSuccess) return cuda_fail(h, ec, "graph capture (launch)");
+            if (e != cudaSuccess) return cuda_fail(h, e, "graph capture (end)");
+            e = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) return cuda_fail(h, e, "graph instantiate");
+            it = h->graphs.emplace(key, exec).first;
+            h->call_launches = save_launches;
+            h->d_zero = dz;
+        }
+        if ((e = cudaGraphLaunch(it->second, h->stream)) != cudaSuccess) return cuda_fail(h, e, "graph launch");
+        h->call_launches += 4 * max_iters;  // kernels in the graph: sigma, transfer, lap2, lap1, lap0
+        h->call_launches += max_iters;
+        h->d_zero = 0;
+        h->b_zero = h->c_zero = 0;
+    } else {
+        for (int t = 0; t < max_iters; t++) {
+            for (int ph = QAP_PHASE_TRANSFER; ph <= QAP_PHASE_CONC_B; ph++) {
+                if (ph == QAP_PHASE_CONC_D) continue;  // enqueued together with TRANSFER
+                if ((e = run_phase(h, ph, h->stream, true)) != cudaSuccess) return cuda_fail(h, e, "iteration");
+            }
         }
     }
     Ctl c;
