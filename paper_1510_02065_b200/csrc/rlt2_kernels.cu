@@ -677,7 +677,7 @@ constexpr unsigned NOIDX = 0xffffffffu;
 enum { TK_LOCAL = 0, TK_AGG = 1, TK_HOLD = 2 };
 
 template <bool SHARDED>
-__global__ void __launch_bounds__(256, 5) k_transfer(const TransferArgs A)
+__global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
 {
     if (A.ctl->stopped) return;
     __shared__ double sv[3][TT * TT * (TT + 1)];  // the three member views of the tile's classes
