@@ -240,16 +240,17 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
             ui0 = nx_u;
             j0 = j1;
         }
-        // augment along way[]: columns on the path take the row (and its u) of way[c]
-        bool onp[CPL];
+        // augment along way[]: columns on the path take the row (and its u) of way[c].
+        // The path (a few columns) is walked once with warp-uniform values; its columns are
+        // collected in a bit mask per column group t.
+        uint32_t onmask[CPL];
 #pragma unroll
-        for (int t = 0; t < CPL; t++) onp[t] = false;
-        int c = jfree;
-        while (c >= 0) {
+        for (int t = 0; t < CPL; t++) onmask[t] = 0u;
+        for (int c = jfree; c >= 0;) {
             const int src = c & 31, tt = c >> 5;
 #pragma unroll
             for (int t = 0; t < CPL; t++)
-                if (lane == src && t == tt) onp[t] = true;
+                if (t == tt) onmask[t] |= 1u << src;
             c = __shfl_sync(FULL_MASK, sel_t<CPL>(way, tt), src);
         }
         int pold[CPL];
@@ -262,7 +263,7 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             const int w = way[t];
-            const int wl = (w < 0 ? 0 : w) & 31, wt = w < 0 ? 0 : (w >> 5);
+            const int wl = w & 31, wt = w >> 5;  // w < 0 (dummy): values unused below
             int np = i * rowb;
             double nu = ucur;
 #pragma unroll
@@ -274,7 +275,7 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
                     nu = su;
                 }
             }
-            if (onp[t]) {
+            if ((onmask[t] >> lane) & 1u) {
                 poff[t] = np;
                 ucol[t] = nu;
             }
@@ -310,14 +311,14 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
         const int c = lane + 32 * t;
         if (c < m) {
             double *Mc = M + c;
-            const int pr = p[t];
             const double vc = v[t];
 #pragma unroll 4
             for (int r = 0; r < m; r++) {
                 const double x = (Mc[r * m] - urow[r]) - vc;
                 mn = x < mn ? x : mn;
-                Mc[r * m] = (x > 0.0 && pr != r) ? x : 0.0;  // x <= 0 (incl. -0) or assigned -> +0
+                Mc[r * m] = x > 0.0 ? x : 0.0;  // x <= 0 (incl. -0) -> +0
             }
+            Mc[p[t] * m] = 0.0;  // assigned cell -> +0
         }
     }
     double S = 0.0;
