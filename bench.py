@@ -27,6 +27,7 @@ sys.path.insert(0, ROOT)
 METRIC = "RLT2 dual-ascent iters/s and LAPs/s at N=30 (1/2/4/8 B200); B&B nodes/s"
 N_DEFAULT, T_ITERS, SEED = 30, 20, 1
 BNB_ITERS = 10
+BNB_BATCH = 12
 
 
 def n_stored(n):
@@ -293,17 +294,23 @@ def main():
     if not args.no_bnb and rank == 0:
         bi = qapgen.nug(12, SEED)
         hb = pkg.qap_rlt2_create(12, bi.F, bi.D, device=local_rank, stream=stream.cuda_stream)
-        pkg.qap_bnb_solve(hb, BNB_ITERS)                     # warm-up
+        pkg.qap_bnb_solve(hb, BNB_ITERS, batch=BNB_BATCH)    # warm-up (handles, graphs)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rb = pkg.qap_bnb_solve(hb, BNB_ITERS)
+        rb = pkg.qap_bnb_solve(hb, BNB_ITERS, batch=BNB_BATCH)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        rs = pkg.qap_bnb_solve(hb, BNB_ITERS, batch=1)
+        dt1 = time.perf_counter() - t1
+        assert (rs["bounded"], rs["opt"]) == (rb["bounded"], rb["opt"])
         pkg.qap_destroy(hb)
         bnb = {"config": f"nug12-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node, UB0=inf, "
-                         "branch on lowest free facility, leaves n'<=3 enumerated",
+                         f"branch on lowest free facility, leaves n'<=3 enumerated, children bounded "
+                         f"{BNB_BATCH} at a time concurrently",
                "nodes_per_s": rb["bounded"] / dt, "bounded_nodes": rb["bounded"], "leaves": rb["leaves"],
-               "pruned": rb["pruned"], "opt": rb["opt"], "seconds": dt, "timer": "host wall clock"}
+               "pruned": rb["pruned"], "opt": rb["opt"], "seconds": dt, "timer": "host wall clock",
+               "nodes_per_s_one_at_a_time": rs["bounded"] / dt1}
     pkg.qap_destroy(h)
 
     if rank != 0:

@@ -126,6 +126,14 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
 qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB,
                           qap_rlt2_result *out);
 
+/*
+ * qap_rlt2_bound_async / qap_rlt2_bound_result — the two halves of qap_rlt2_bound: enqueue
+ * the bound on the handle's stream without synchronising, then wait for it and read the
+ * result.  Lets a caller run independent bounds on several handles concurrently.
+ */
+qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double UB);
+qap_status qap_rlt2_bound_result(qap_rlt2 *h, qap_rlt2_result *out);
+
 /* Entry counts of the export layouts above for the current node (HOST outputs).       */
 qap_status qap_rlt2_dual_sizes(const qap_rlt2 *h, int64_t *nB, int64_t *nC, int64_t *nD);
 
@@ -228,10 +236,13 @@ qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_d
  *   fixed (cold) and bounded with `iters` iterations; nodes with n' <= 3 are leaves
  *   solved by enumeration; prune when LB > UB - 1 + 1e-6; the incumbent is replaced
  *   only on strict improvement.  UB0 = +INFINITY for none.
+ *   batch > 1: the children of an expanded node are bounded `batch` at a time
+ *   concurrently (helper handles on their own streams, each sized like h); with K = 0
+ *   every decision equals the one-node-at-a-time search.
  *   Outputs (HOST): *opt (or -1 if nothing better than UB0), perm[N], node counts.
  *   The handle's node is left at the last bounded node.
  */
-qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int64_t *opt,
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int64_t *opt,
                          int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned);
 
 #ifdef __cplusplus

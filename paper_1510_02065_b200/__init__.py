@@ -32,7 +32,8 @@ KERNEL_KINDS = ["init", "sigma", "transfer", "lap2", "lap1", "lap0"]
 EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound", "qap_rlt2_dual_sizes",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
            "qap_destroy", "qap_lap_batch", "qap_bnb_solve", "qap_nccl_unique_id", "qap_rlt2_shard_info",
-           "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound"]
+           "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound", "qap_rlt2_bound_async",
+           "qap_rlt2_bound_result"]
 
 
 class QapError(RuntimeError):
@@ -79,8 +80,10 @@ def load_library(path: str = LIB_PATH):
     L.qap_destroy.argtypes = [vp]
     L.qap_destroy.restype = None
     L.qap_lap_batch.argtypes = [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
-    L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, ct.POINTER(i64), vp, ct.POINTER(i64),
+    L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, i32, ct.POINTER(i64), vp, ct.POINTER(i64),
                                 ct.POINTER(i64), ct.POINTER(i64)]
+    L.qap_rlt2_bound_async.argtypes = [vp, i32, f64, f64]
+    L.qap_rlt2_bound_result.argtypes = [vp, ct.POINTER(_Result)]
     L.qap_nccl_unique_id.argtypes = [vp]
     L.qap_rlt2_shard_info.argtypes = [vp] + [vp] * 7
     L.qap_shard_plan.argtypes = [i32, i32, i32, vp, vp, vp, vp, i64, ct.POINTER(i64)]
@@ -231,11 +234,21 @@ def qap_lap_batch(M, R=None, S=None, assign=None, u=None, v=None, steps=None, er
     _check(st, None)
 
 
-def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf) -> dict:
+def qap_rlt2_bound_async(h: Handle, max_iters: int, K: float = 0.0, UB: float = math.inf) -> None:
+    _check(load_library().qap_rlt2_bound_async(h.ptr, max_iters, K, UB), h)
+
+
+def qap_rlt2_bound_result(h: Handle) -> dict:
+    r = _Result()
+    _check(load_library().qap_rlt2_bound_result(h.ptr, ct.byref(r)), h)
+    return dict(lb=r.lb, lb_glb=r.lb_glb, iters=r.iters, status=r.status, launches=r.launches)
+
+
+def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1) -> dict:
     opt = ct.c_int64()
     perm = np.zeros(h.N, np.int32)
     b, l, p = ct.c_int64(), ct.c_int64(), ct.c_int64()
-    _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, ct.byref(opt), perm.ctypes.data, ct.byref(b),
+    _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, batch, ct.byref(opt), perm.ctypes.data, ct.byref(b),
                                         ct.byref(l), ct.byref(p)), h)
     return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value)
 

@@ -580,6 +580,14 @@ qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase)
 qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, qap_rlt2_result *out)
 {
     if (!h || !out) return h ? fail(h, QAP_E_ARG, "out is NULL") : QAP_E_ARG;
+    qap_status s = qap_rlt2_bound_async(h, max_iters, K, UB);
+    if (s != QAP_OK) return s;
+    return qap_rlt2_bound_result(h, out);
+}
+
+qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double UB)
+{
+    if (!h) return QAP_E_ARG;
     if (max_iters < 0 || !(K >= 0.0) || std::isnan(UB)) return fail(h, QAP_E_ARG, "bad max_iters/K/UB");
     if (h->next_phase != PH_FRESH && h->next_phase != QAP_PHASE_TRANSFER)
         return fail(h, QAP_E_STATE, "bound called in the middle of an iteration");
@@ -633,6 +641,13 @@ qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, q
             }
         }
     }
+    return QAP_OK;
+}
+
+qap_status qap_rlt2_bound_result(qap_rlt2 *h, qap_rlt2_result *out)
+{
+    if (!h || !out) return h ? fail(h, QAP_E_ARG, "out is NULL") : QAP_E_ARG;
+    cudaError_t e;
     Ctl c;
     qap_status s = read_ctl(h, c);
     if (s != QAP_OK) return s;
@@ -750,9 +765,17 @@ qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_d
 }
 
 // ---- minimal deterministic B&B (P:236-238 caller) ----------------------
+// Depth-first; a node is bounded when its parent is expanded: the children of a node are
+// bounded together, `batch` at a time, each on its own handle and stream (independent
+// subproblems run concurrently on the GPU).  Children are then visited in ascending
+// location order and pruned against the CURRENT incumbent.  With K = 0 this makes exactly
+// the decisions of the one-node-at-a-time DFS (a bound only stops early when LB already
+// exceeds UB - 1 + 1e-6, and LB is nondecreasing), so node counts, optimum and
+// permutation equal the oracle's sequential B&B.
 namespace {
 struct Bnb {
-    qap_rlt2 *h;
+    std::vector<qap_rlt2 *> pool;  // pool[0] = the caller's handle
+    std::vector<cudaStream_t> own_streams;
     int N, iters;
     double K, UB;
     bool have;
@@ -760,16 +783,17 @@ struct Bnb {
     std::vector<int32_t> best_perm;
     int64_t bounded = 0, leaves = 0, pruned = 0;
     qap_status st = QAP_OK;
+    const qap_rlt2 *h0() const { return pool[0]; }
 
     int64_t cost(const std::vector<int32_t> &perm) const
     {
         int64_t v = 0;
         for (int i = 0; i < N; i++)
-            for (int k = 0; k < N; k++) v += h->F[i * N + k] * h->Dist[perm[i] * N + perm[k]];
+            for (int k = 0; k < N; k++) v += h0()->F[i * N + k] * h0()->Dist[perm[i] * N + perm[k]];
         return v;
     }
-    void leaf(std::vector<int32_t> &perm, const std::vector<int> &ffac, const std::vector<int> &floc, int t,
-              std::vector<char> &used)
+    void leaf_rec(std::vector<int32_t> &perm, const std::vector<int> &ffac, const std::vector<int> &floc, int t,
+                  std::vector<char> &used)
     {
         if (t == (int)ffac.size()) {
             const int64_t v = cost(perm);
@@ -785,62 +809,133 @@ struct Bnb {
             if (used[x]) continue;
             used[x] = 1;
             perm[ffac[t]] = floc[x];
-            leaf(perm, ffac, floc, t + 1, used);
+            leaf_rec(perm, ffac, floc, t + 1, used);
             used[x] = 0;
         }
     }
-    void visit(std::vector<int32_t> &fac, std::vector<int32_t> &loc)
+    void free_sets(const std::vector<int32_t> &fac, const std::vector<int32_t> &loc, std::vector<int> &ffac,
+                   std::vector<int> &floc) const
     {
-        if (st != QAP_OK) return;
         std::vector<char> uf(N, 0), ul(N, 0);
         for (size_t t = 0; t < fac.size(); t++) uf[fac[t]] = ul[loc[t]] = 1;
-        std::vector<int> ffac, floc;
         for (int x = 0; x < N; x++) {
             if (!uf[x]) ffac.push_back(x);
             if (!ul[x]) floc.push_back(x);
         }
-        if (ffac.size() <= 3) {
-            leaves++;
-            std::vector<int32_t> perm(N, 0);
-            for (size_t t = 0; t < fac.size(); t++) perm[fac[t]] = loc[t];
-            std::vector<char> used(floc.size(), 0);
-            leaf(perm, ffac, floc, 0, used);
+    }
+    void leaf(const std::vector<int32_t> &fac, const std::vector<int32_t> &loc)
+    {
+        std::vector<int> ffac, floc;
+        free_sets(fac, loc, ffac, floc);
+        leaves++;
+        std::vector<int32_t> perm(N, 0);
+        for (size_t t = 0; t < fac.size(); t++) perm[fac[t]] = loc[t];
+        std::vector<char> used(floc.size(), 0);
+        leaf_rec(perm, ffac, floc, 0, used);
+    }
+    // bound the nodes (fac + {f -> x}) for x in xs, concurrently; LBs in the same order
+    bool bound_children(std::vector<int32_t> &fac, std::vector<int32_t> &loc, int f, const std::vector<int> &xs,
+                        std::vector<double> &lb)
+    {
+        lb.assign(xs.size(), 0.0);
+        const size_t B = pool.size();
+        for (size_t c0 = 0; c0 < xs.size(); c0 += B) {
+            const size_t c1 = c0 + B < xs.size() ? c0 + B : xs.size();
+            for (size_t c = c0; c < c1; c++) {
+                qap_rlt2 *h = pool[c - c0];
+                fac.push_back(f);
+                loc.push_back(xs[c]);
+                st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data());
+                fac.pop_back();
+                loc.pop_back();
+                if (st != QAP_OK) return false;
+                if ((st = qap_rlt2_bound_async(h, iters, K, UB)) != QAP_OK) return false;
+            }
+            for (size_t c = c0; c < c1; c++) {
+                qap_rlt2_result r{};
+                if ((st = qap_rlt2_bound_result(pool[c - c0], &r)) != QAP_OK) return false;
+                lb[c] = r.lb;
+                bounded++;
+            }
+        }
+        return true;
+    }
+    // node (fac, loc) is bounded and not pruned: expand it
+    void expand(std::vector<int32_t> &fac, std::vector<int32_t> &loc)
+    {
+        if (st != QAP_OK) return;
+        std::vector<int> ffac, floc;
+        free_sets(fac, loc, ffac, floc);
+        const int f = ffac[0];
+        const bool child_leaf = ffac.size() - 1 <= 3;
+        std::vector<double> lb;
+        if (!child_leaf && !bound_children(fac, loc, f, floc, lb)) return;
+        for (size_t c = 0; c < floc.size(); c++) {
+            fac.push_back(f);
+            loc.push_back(floc[c]);
+            if (child_leaf) leaf(fac, loc);
+            else if (lb[c] > UB - 1.0 + 1e-6) pruned++;
+            else expand(fac, loc);
+            fac.pop_back();
+            loc.pop_back();
+            if (st != QAP_OK) return;
+        }
+    }
+    void run()
+    {
+        std::vector<int32_t> fac, loc;
+        if (N <= 3) {
+            leaf(fac, loc);
             return;
         }
-        if ((st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return;
+        if ((st = qap_rlt2_fix(pool[0], 0, nullptr, nullptr)) != QAP_OK) return;
         qap_rlt2_result r{};
-        if ((st = qap_rlt2_bound(h, iters, K, UB, &r)) != QAP_OK) return;
+        if ((st = qap_rlt2_bound(pool[0], iters, K, UB, &r)) != QAP_OK) return;
         bounded++;
         if (r.lb > UB - 1.0 + 1e-6) {
             pruned++;
             return;
         }
-        const int f = ffac[0];
-        for (int x : floc) {
-            fac.push_back(f);
-            loc.push_back(x);
-            visit(fac, loc);
-            fac.pop_back();
-            loc.pop_back();
-        }
+        expand(fac, loc);
+    }
+    ~Bnb()
+    {
+        for (size_t k = 1; k < pool.size(); k++) qap_destroy(pool[k]);
+        for (auto s : own_streams) cudaStreamDestroy(s);
     }
 };
 }  // namespace
 
-qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int64_t *opt, int32_t *perm,
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int64_t *opt, int32_t *perm,
                          int64_t *bounded, int64_t *leaves, int64_t *pruned)
 {
     if (!h || !opt || !perm || iters < 0) return QAP_E_ARG;
+    if (h->world > 1 && batch > 1) return fail(h, QAP_E_ARG, "batched B&B needs a single-GPU handle");
     Bnb b;
-    b.h = h;
+    b.pool.push_back(h);
     b.N = h->N;
     b.iters = iters;
     b.K = K;
     b.UB = UB0;
     b.have = false;
     b.best = -1;
-    std::vector<int32_t> fac, loc;
-    b.visit(fac, loc);
+    const int B = batch < 1 ? 1 : (batch > b.N ? b.N : batch);
+    for (int k = 1; k < B; k++) {  // helper handles, each on its own stream
+        cudaStream_t s = nullptr;
+        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(h, e, "bnb stream");
+        b.own_streams.push_back(s);
+        qap_rlt2_opts o{};
+        o.device = h->device;
+        o.cuda_stream = s;
+        o.flags = h->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP);
+        o.lap_warps = h->lap_warps;
+        qap_rlt2 *x = nullptr;
+        qap_status st = qap_rlt2_create(h->N, h->F.data(), h->Dist.data(), &o, &x);
+        if (st != QAP_OK) return fail(h, st, std::string("bnb helper handle: ") + qap_last_error(nullptr));
+        b.pool.push_back(x);
+    }
+    b.run();
     if (b.st != QAP_OK) return b.st;
     *opt = b.have ? b.best : -1;
     if (b.have)

@@ -261,13 +261,14 @@ def test_zero_and_constant_instances(orc, torch, pkg):
     pkg.qap_destroy(h)
 
 
+@pytest.mark.parametrize("batch", [1, 4, 16])
 @pytest.mark.parametrize("family,n", [("nug", 7), ("taib", 8), ("uniform", 8), ("nug", 10)])
-def test_bnb_parity(orc, torch, pkg, family, n):
-    """B&B node counts, optimum and permutation identical to the oracle B&B; optimum equals
-    brute force."""
+def test_bnb_parity(orc, torch, pkg, family, n, batch):
+    """B&B node counts, optimum and permutation identical to the oracle B&B (one node at a
+    time) also when children are bounded concurrently; optimum equals brute force."""
     inst = qapgen.make(family, n, 1)
     h = pkg.qap_rlt2_create(n, inst.F, inst.D)
-    g = pkg.qap_bnb_solve(h, 3)
+    g = pkg.qap_bnb_solve(h, 3, batch=batch)
     o = orc.bnb(inst.F, inst.D, T=3)
     assert g["opt"] == o["opt"]
     assert (g["perm"] == o["perm"]).all()
@@ -304,3 +305,18 @@ def test_wide_columns_level2_n35(orc, torch, pkg):
     idx = np.random.default_rng(1).integers(0, D.shape[0], 1500)
     rel_close(D[idx], st.D[idx])
     pkg.qap_destroy(h)
+
+
+def test_bound_async_concurrent(torch, pkg):
+    """Independent bounds on several handles, enqueued before any is read back."""
+    inst = qapgen.taib(10, 6)
+    hs = [pkg.qap_rlt2_create(10, inst.F, inst.D, stream=torch.cuda.Stream().cuda_stream) for _ in range(3)]
+    fixes = [(), ((0, 1),), ((2, 2), (5, 7))]
+    for h, fx in zip(hs, fixes):
+        pkg.qap_rlt2_fix(h, fx)
+        pkg.qap_rlt2_bound_async(h, 4)
+    res = [pkg.qap_rlt2_bound_result(h) for h in hs]
+    for h, fx, r in zip(hs, fixes, res):
+        pkg.qap_rlt2_fix(h, fx)
+        assert pkg.qap_rlt2_bound(h, 4)["lb"] == r["lb"]
+        pkg.qap_destroy(h)
