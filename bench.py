@@ -304,13 +304,20 @@ def main():
         rs = pkg.qap_bnb_solve(hb, BNB_ITERS, batch=1)
         dt1 = time.perf_counter() - t1
         assert (rs["bounded"], rs["opt"]) == (rb["bounded"], rb["opt"])
+        t2 = time.perf_counter()
+        rsb = pkg.qap_bnb_solve(hb, BNB_ITERS, batch=BNB_BATCH, sb_iters=1)
+        dt2 = time.perf_counter() - t2
+        assert rsb["opt"] == rb["opt"]
         pkg.qap_destroy(hb)
         bnb = {"config": f"nug12-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node, UB0=inf, "
                          f"branch on lowest free facility, leaves n'<=3 enumerated, children bounded "
                          f"{BNB_BATCH} at a time concurrently",
                "nodes_per_s": rb["bounded"] / dt, "bounded_nodes": rb["bounded"], "leaves": rb["leaves"],
                "pruned": rb["pruned"], "opt": rb["opt"], "seconds": dt, "timer": "host wall clock",
-               "nodes_per_s_one_at_a_time": rs["bounded"] / dt1}
+               "nodes_per_s_one_at_a_time": rs["bounded"] / dt1,
+               "strong_branching": {"sb_iters": 1, "bounded_nodes": rsb["bounded"], "leaves": rsb["leaves"],
+                                    "cut_by_rlt1": rsb["sb_cut"], "seconds": dt2,
+                                    "nodes_per_s": rsb["bounded"] / dt2}}
     pkg.qap_destroy(h)
 
     if rank != 0:

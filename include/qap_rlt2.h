@@ -238,12 +238,29 @@ qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_d
  *   only on strict improvement.  UB0 = +INFINITY for none.
  *   batch > 1: the children of an expanded node are bounded `batch` at a time
  *   concurrently (helper handles on their own streams, each sized like h); with K = 0
- *   every decision equals the one-node-at-a-time search (see DESIGN.md §9b).
+ *   every decision equals the one-node-at-a-time search (DESIGN.md §9).
+ *   sb_iters >= 0: strong branching at nodes with n' >= 5: the line chosen by
+ *   qap_rlt2_strong_branch is branched on (children in ascending order of the line's other
+ *   index) and candidates whose RLT1 estimate exceeds UB - 1 + 1e-6 are cut (*sb_cut).
  *   Outputs (HOST): *opt (or -1 if nothing better than UB0), perm[N], node counts.
  *   The handle's node is left at the last bounded node.
  */
-qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int64_t *opt,
-                         int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned);
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int32_t sb_iters,
+                         int64_t *opt, int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned,
+                         int64_t *sb_cut);
+
+/*
+ * qap_rlt2_strong_branch — strong branching with the RLT1 dual: every candidate
+ *   child of the handle's current node (free facility I[a] at free location J[b], reduced
+ *   indices, n = free facilities >= 4) is bounded by a cold RLT1 ascent (Algorithm 1 without
+ *   the D operations; iteration 0 + sb_iters iterations of spread B->C, C pair mean,
+ *   concentrate C->B, concentrate B->LB), all children at once on the GPU.
+ *   est (HOST, n*n): est[a*n + b] = kappa_child + RLT1 bound.  *kind = 0 (row a) or
+ *   1 (column b), *index = the line with the maximal min-estimate (ties: lowest index,
+ *   rows first).  Uses a separate workspace (~ n^2 * 8 (n-1)^2 (n-2)^2 bytes); the node's
+ *   own dual state is untouched.  Synchronises the stream.
+ */
+qap_status qap_rlt2_strong_branch(qap_rlt2 *h, int32_t sb_iters, double *est, int32_t *kind, int32_t *index);
 
 #ifdef __cplusplus
 }

@@ -77,9 +77,13 @@ def lib():
             getattr(L, f).argtypes = [ct.c_void_p]
             getattr(L, f).restype = ct.POINTER(ct.c_double)
         L.oracle_state_free_maps.argtypes = [ct.c_void_p, _i32p, _i32p]
-        L.oracle_bnb.argtypes = [ct.c_int, _i64p, _i64p, ct.c_int, ct.c_double, ct.c_double,
+        L.oracle_bnb.argtypes = [ct.c_int, _i64p, _i64p, ct.c_int, ct.c_double, ct.c_double, ct.c_int,
                                  ct.POINTER(ct.c_int64), _i32p, ct.POINTER(ct.c_int64),
-                                 ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]
+                                 ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]
+        L.oracle_rlt1_iteration.argtypes = [ct.c_void_p, ct.POINTER(ct.c_double)]
+        L.oracle_rlt1_bound.argtypes = [ct.c_void_p, ct.c_int, ct.POINTER(ct.c_double)]
+        L.oracle_strong_branch.argtypes = [ct.c_int, _i64p, _i64p, ct.c_int, _i32p, _i32p, ct.c_int, _f64p,
+                                           ct.POINTER(ct.c_int), ct.POINTER(ct.c_int)]
         _lib = L
     return _lib
 
@@ -163,6 +167,16 @@ class State:
         _check(self._L.oracle_concentrate_b(self._h, ct.byref(x)), "concentrate_b")
         return x.value
 
+    def rlt1_iteration(self) -> float:
+        x = ct.c_double()
+        _check(self._L.oracle_rlt1_iteration(self._h, ct.byref(x)), "rlt1_iteration")
+        return x.value
+
+    def rlt1_bound(self, T: int) -> float:
+        x = ct.c_double()
+        _check(self._L.oracle_rlt1_bound(self._h, T, ct.byref(x)), "rlt1_bound")
+        return x.value
+
     def iteration(self) -> float:
         x = ct.c_double()
         _check(self._L.oracle_iteration(self._h, ct.byref(x)), "iteration")
@@ -232,17 +246,34 @@ def bound(F, Dist, T: int, K: float = 0.0, UB: float = math.inf, fixed=(), trace
     return s.bound(T, K, UB, trace=trace)
 
 
-def bnb(F, Dist, T: int = 3, K: float = 0.0, UB0: float = math.inf):
-    """Minimal deterministic DFS branch-and-bound; returns dict(opt, perm, bounded, leaves, pruned)."""
+def bnb(F, Dist, T: int = 3, K: float = 0.0, UB0: float = math.inf, sb_iters: int = -1):
+    """Minimal deterministic DFS branch-and-bound (strong branching with RLT1 when
+    sb_iters >= 0); returns dict(opt, perm, bounded, leaves, pruned, sb_cut)."""
     F = np.ascontiguousarray(F, dtype=np.int64)
     Dist = np.ascontiguousarray(Dist, dtype=np.int64)
     N = F.shape[0]
     best = ct.c_int64()
     perm = np.zeros(N, np.int32)
-    b, l, p = ct.c_int64(), ct.c_int64(), ct.c_int64()
-    _check(lib().oracle_bnb(N, F, Dist, T, K, UB0, ct.byref(best), perm, ct.byref(b), ct.byref(l),
-                            ct.byref(p)), "bnb")
-    return dict(opt=best.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value)
+    b, l, p, c = ct.c_int64(), ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(lib().oracle_bnb(N, F, Dist, T, K, UB0, sb_iters, ct.byref(best), perm, ct.byref(b), ct.byref(l),
+                            ct.byref(p), ct.byref(c)), "bnb")
+    return dict(opt=best.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
+
+
+def strong_branch(F, Dist, fixed=(), T: int = 1):
+    """RLT1 estimates est[a, b] of every candidate child and the selected line (kind 0 = row /
+    1 = column, reduced index)."""
+    F = np.ascontiguousarray(F, dtype=np.int64)
+    Dist = np.ascontiguousarray(Dist, dtype=np.int64)
+    N = F.shape[0]
+    n = N - len(fixed)
+    fac = np.array([a for a, _ in fixed] or [0], dtype=np.int32)
+    loc = np.array([b for _, b in fixed] or [0], dtype=np.int32)
+    est = np.zeros(n * n, np.float64)
+    kind, index = ct.c_int(), ct.c_int()
+    _check(lib().oracle_strong_branch(N, F, Dist, len(fixed), fac, loc, T, est, ct.byref(kind), ct.byref(index)),
+           "strong_branch")
+    return est.reshape(n, n), kind.value, index.value
 
 
 def block_list(n: int):

@@ -471,6 +471,81 @@ int oracle_bound(ostate *s, int T, double K, double UB, double *lb_out, double *
     return ORC_OK;
 }
 
+/*
+ * RLT1 dual ascent ("the costs concentration follows the RLT1 dual algorithm similar to
+ * Section 4, except by the operations with transfer costs of D matrix"):
+ * iteration 0 as above, then per iteration: spread B->C, transfer between the
+ * complementary costs of C (pair mean, reading R13 — NOT a no-op here), concentrate
+ * C->B, concentrate B->LB.  D is neither read nor written.
+ */
+int oracle_rlt1_iteration(ostate *s, double *lbprime)
+{
+    int st;
+    if ((st = oracle_spread_b(s))) return st;
+    if ((st = oracle_transfer_c(s))) return st;
+    if ((st = oracle_concentrate_c(s))) return st;
+    return oracle_concentrate_b(s, lbprime);
+}
+
+int oracle_rlt1_bound(ostate *s, int T, double *lb_out)
+{
+    int st;
+    if (s->fresh && (st = oracle_iteration0(s))) return st;
+    for (int t = 0; t < T; t++) {
+        double lbp;
+        if ((st = oracle_rlt1_iteration(s, &lbp))) return st;
+    }
+    *lb_out = (double)s->kappa + s->lb_dual;
+    return ORC_OK;
+}
+
+/*
+ * Strong branching: estimate every candidate child (free facility I[a] at free
+ * location J[b]) of the node Φ = (fac, loc) by a cold RLT1 bound with T iterations
+ * (est[a*n + b], n = N - nfix), then score each row a by min_b est and each column b by
+ * min_a est and select the line with the MAXIMUM score (SPEC S:374-382 max-min reading;
+ * ties: lowest index, row preferred over column).  *kind = 0 row / 1 column, *index =
+ * reduced index of the line.  Requires n >= 4 (children have >= 3 free facilities).
+ */
+int oracle_strong_branch(int N, const int64_t *F, const int64_t *Dist, int nfix, const int32_t *fac,
+                         const int32_t *loc, int T, double *est, int *kind, int *index)
+{
+    int n = N - nfix;
+    if (n < 4) return ORC_E_ARG;
+    char uf[64] = {0}, ul[64] = {0};
+    for (int t = 0; t < nfix; t++) { uf[fac[t]] = 1; ul[loc[t]] = 1; }
+    int32_t I[64], J[64];
+    int ni = 0, nj = 0;
+    for (int x = 0; x < N; x++) { if (!uf[x]) I[ni++] = x; if (!ul[x]) J[nj++] = x; }
+    int32_t cf[64], cl[64];
+    for (int t = 0; t < nfix; t++) { cf[t] = fac[t]; cl[t] = loc[t]; }
+    for (int a = 0; a < n; a++)
+        for (int b = 0; b < n; b++) {
+            cf[nfix] = I[a];
+            cl[nfix] = J[b];
+            int err;
+            ostate *s = oracle_state_new(N, F, Dist, nfix + 1, cf, cl, &err);
+            if (!s) return err;
+            int st = oracle_rlt1_bound(s, T, &est[a * n + b]);
+            oracle_state_free(s);
+            if (st) return st;
+        }
+    double best = -INFINITY;
+    *kind = 0;
+    *index = 0;
+    for (int a = 0; a < n; a++) {          /* rows first: a row wins exact ties with a column */
+        double sc = INFINITY;
+        for (int b = 0; b < n; b++) if (est[a * n + b] < sc) sc = est[a * n + b];
+        if (sc > best) { best = sc; *kind = 0; *index = a; }
+    }
+    for (int b = 0; b < n; b++) {
+        double sc = INFINITY;
+        for (int a = 0; a < n; a++) if (est[a * n + b] < sc) sc = est[a * n + b];
+        if (sc > best) { best = sc; *kind = 1; *index = b; }
+    }
+    return ORC_OK;
+}
+
 /* ---- accessors for the Python wrapper -------------------------------------- */
 int oracle_state_n(const ostate *s) { return s->n; }
 int64_t oracle_state_kappa(const ostate *s) { return s->kappa; }
@@ -496,7 +571,8 @@ void oracle_state_free_maps(const ostate *s, int32_t *I, int32_t *J)
  * location order (reading R20); cold children (reading R19): every node is
  * reduced and initialised from scratch, then bounded with T iterations (R18).
  * Nodes with n' <= 3 free facilities are leaves solved by enumerating completions
- * in lexicographic order.  A node is pruned when LB > UB - 1 + 1e-6 (optima are
+ * in lexicographic order.  Optional strong branching (sb_iters >= 0) at nodes with
+ * n' >= 5: see oracle_strong_branch; children in ascending order of the line's other index.  A node is pruned when LB > UB - 1 + 1e-6 (optima are
  * integral, reading R15); the incumbent is replaced only on strict improvement
  * (reading R22).
  */
@@ -504,6 +580,8 @@ typedef struct {
     int N;
     const int64_t *F, *Dist;
     int T;
+    int sb_iters;        /* >= 0: strong branching with RLT1 (sb_iters iterations); < 0: off */
+    int64_t sb_cut;      /* candidates cut by their RLT1 estimate                          */
     double K;
     int64_t best;        /* incumbent value; INT64_MAX = none             */
     int have_best;
@@ -567,6 +645,22 @@ static void bnb_visit(bnb_ctx *c, int nfix, int32_t *fac, int32_t *loc)
     if (st) { c->err = st; return; }
     c->bounded++;
     if (LB > c->UB - 1.0 + 1e-6) { c->pruned++; return; }
+    if (c->sb_iters >= 0 && nf >= 5) {
+        /* strong branching: branch on the row or column with the highest min-estimate;
+           candidates whose RLT1 estimate already exceeds the incumbent are cut */
+        double *est = malloc(sizeof(double) * nf * nf);
+        int kind, index;
+        int st2 = oracle_strong_branch(N, c->F, c->Dist, nfix, fac, loc, c->sb_iters, est, &kind, &index);
+        if (st2) { free(est); c->err = st2; return; }
+        for (int x = 0; x < nf; x++) {
+            const int a = kind == 0 ? index : x, b = kind == 0 ? x : index;
+            if (est[a * nf + b] > c->UB - 1.0 + 1e-6) { c->sb_cut++; continue; }
+            fac[nfix] = ffac[a]; loc[nfix] = floc[b];
+            bnb_visit(c, nfix + 1, fac, loc);
+        }
+        free(est);
+        return;
+    }
     int f = ffac[0];
     for (int x = 0; x < nl; x++) {
         fac[nfix] = f; loc[nfix] = floc[x];
@@ -574,19 +668,20 @@ static void bnb_visit(bnb_ctx *c, int nfix, int32_t *fac, int32_t *loc)
     }
 }
 
-int oracle_bnb(int N, const int64_t *F, const int64_t *Dist, int T, double K, double UB0,
+int oracle_bnb(int N, const int64_t *F, const int64_t *Dist, int T, double K, double UB0, int sb_iters,
                int64_t *best_out, int32_t *perm_out, int64_t *bounded_out, int64_t *leaves_out,
-               int64_t *pruned_out)
+               int64_t *pruned_out, int64_t *sb_cut_out)
 {
     if (N < 1 || N > 64) return ORC_E_ARG;
     bnb_ctx c;
     memset(&c, 0, sizeof c);
-    c.N = N; c.F = F; c.Dist = Dist; c.T = T; c.K = K; c.UB = UB0;
+    c.N = N; c.F = F; c.Dist = Dist; c.T = T; c.K = K; c.UB = UB0; c.sb_iters = sb_iters;
     int32_t fac[64], loc[64];
     bnb_visit(&c, 0, fac, loc);
     if (c.err) return c.err;
     *best_out = c.have_best ? c.best : -1;
     if (c.have_best) memcpy(perm_out, c.best_perm, sizeof(int32_t) * N);
     *bounded_out = c.bounded; *leaves_out = c.leaves; *pruned_out = c.pruned;
+    if (sb_cut_out) *sb_cut_out = c.sb_cut;
     return ORC_OK;
 }

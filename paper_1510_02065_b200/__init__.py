@@ -33,7 +33,7 @@ EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
            "qap_destroy", "qap_lap_batch", "qap_bnb_solve", "qap_nccl_unique_id", "qap_rlt2_shard_info",
            "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound", "qap_rlt2_bound_async",
-           "qap_rlt2_bound_result"]
+           "qap_rlt2_bound_result", "qap_rlt2_strong_branch"]
 
 
 class QapError(RuntimeError):
@@ -80,8 +80,9 @@ def load_library(path: str = LIB_PATH):
     L.qap_destroy.argtypes = [vp]
     L.qap_destroy.restype = None
     L.qap_lap_batch.argtypes = [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]
-    L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, i32, ct.POINTER(i64), vp, ct.POINTER(i64),
-                                ct.POINTER(i64), ct.POINTER(i64)]
+    L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, i32, i32, ct.POINTER(i64), vp, ct.POINTER(i64),
+                                ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
+    L.qap_rlt2_strong_branch.argtypes = [vp, i32, vp, ct.POINTER(i32), ct.POINTER(i32)]
     L.qap_rlt2_bound_async.argtypes = [vp, i32, f64, f64]
     L.qap_rlt2_bound_result.argtypes = [vp, ct.POINTER(_Result)]
     L.qap_nccl_unique_id.argtypes = [vp]
@@ -244,13 +245,26 @@ def qap_rlt2_bound_result(h: Handle) -> dict:
     return dict(lb=r.lb, lb_glb=r.lb_glb, iters=r.iters, status=r.status, launches=r.launches)
 
 
-def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1) -> dict:
+def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
+                  sb_iters: int = -1) -> dict:
     opt = ct.c_int64()
     perm = np.zeros(h.N, np.int32)
-    b, l, p = ct.c_int64(), ct.c_int64(), ct.c_int64()
-    _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, batch, ct.byref(opt), perm.ctypes.data, ct.byref(b),
-                                        ct.byref(l), ct.byref(p)), h)
-    return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value)
+    b, l, p, c = ct.c_int64(), ct.c_int64(), ct.c_int64(), ct.c_int64()
+    _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, batch, sb_iters, ct.byref(opt), perm.ctypes.data,
+                                        ct.byref(b), ct.byref(l), ct.byref(p), ct.byref(c)), h)
+    return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
+
+
+def qap_rlt2_strong_branch(h: Handle, sb_iters: int = 1):
+    """RLT1 estimates of every candidate child of the current node (n×n) and the chosen line
+    (kind 0 = row / 1 = column, reduced index)."""
+    B, _, _ = qap_rlt2_dual_sizes(h)
+    n = int(round(B ** 0.5))
+    est = np.zeros(n * n, np.float64)
+    kind, index = ct.c_int32(), ct.c_int32()
+    _check(load_library().qap_rlt2_strong_branch(h.ptr, sb_iters, est.ctypes.data, ct.byref(kind),
+                                                 ct.byref(index)), h)
+    return est.reshape(n, n), kind.value, index.value
 
 
 def qap_nccl_unique_id() -> bytes:

@@ -67,6 +67,12 @@ struct qap_rlt2 {
     size_t tiles_cap = 0, slots_cap = 0;
     int64_t dblk_cap = 0;     // stored blocks the D allocation can hold
     double *dSend = nullptr, *dRecv = nullptr, *dSall = nullptr;
+    // strong-branching workspace (RLT1 children of a node), grown on demand
+    double *dRc = nullptr, *dRb = nullptr, *dRlbd = nullptr;
+    long long *dRkap = nullptr;
+    size_t rc_cap = 0, rb_cap = 0, rk_cap = 0;
+    std::vector<double> h_lbd;
+    std::vector<long long> h_kap;
     // CUDA graphs of the iteration loop, keyed by (n, iterations, D still zero)
     cudaStream_t sCap = nullptr;
     std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
@@ -149,6 +155,10 @@ static void free_all(qap_rlt2 *h)
     if (h->evJoin) cudaEventDestroy(h->evJoin);
     if (h->evS) cudaEventDestroy(h->evS);
     if (h->evL) cudaEventDestroy(h->evL);
+    cudaFree(h->dRc);
+    cudaFree(h->dRb);
+    cudaFree(h->dRlbd);
+    cudaFree(h->dRkap);
     for (auto &kv : h->graphs) cudaGraphExecDestroy(kv.second);
     h->graphs.clear();
     if (h->sCap) cudaStreamDestroy(h->sCap);
@@ -664,6 +674,84 @@ qap_status qap_rlt2_bound_result(qap_rlt2 *h, qap_rlt2_result *out)
     return QAP_OK;
 }
 
+static cudaError_t grow(void **p, size_t &cap, size_t bytes)
+{
+    if (bytes <= cap) return cudaSuccess;
+    cudaFree(*p);
+    *p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+}
+
+qap_status qap_rlt2_strong_branch(qap_rlt2 *h, int32_t sb_iters, double *est, int32_t *kind, int32_t *index)
+{
+    if (!h || !est || !kind || !index || sb_iters < 0) return QAP_E_ARG;
+    const int n = h->node.n;
+    if (n < 4) return fail(h, QAP_E_ARG, "strong branching needs n >= 4 free facilities");
+    Rlt1Batch R{};
+    R.K = n * n;
+    make_geom(n - 1, R.g);
+    R.bstr = ((int64_t)(n - 1) * (n - 1) + 1) & ~int64_t(1);
+    cudaError_t e;
+    if ((e = grow(reinterpret_cast<void **>(&h->dRc), h->rc_cap, (size_t)R.K * (n - 1) * (n - 1) * R.g.ldc * 8)) ||
+        (e = grow(reinterpret_cast<void **>(&h->dRb), h->rb_cap, (size_t)R.K * R.bstr * 8 + 16)) ||
+        (e = grow(reinterpret_cast<void **>(&h->dRlbd), h->rk_cap, (size_t)R.K * 8)))
+        return e == cudaErrorMemoryAllocation ? fail(h, QAP_E_CAPACITY, "strong-branching workspace")
+                                              : cuda_fail(h, e, "strong-branching workspace");
+    if (!h->dRkap || h->h_kap.size() < (size_t)R.K) {
+        cudaFree(h->dRkap);
+        h->dRkap = nullptr;
+        if ((e = cudaMalloc(reinterpret_cast<void **>(&h->dRkap), (size_t)R.K * 8)) != cudaSuccess)
+            return cuda_fail(h, e, "strong-branching workspace");
+        h->h_kap.resize(R.K);
+    }
+    h->h_lbd.resize(R.K);
+    R.C = h->dRc;
+    R.B = h->dRb;
+    R.lbd = h->dRlbd;
+    R.kap = h->dRkap;
+    cudaStream_t st = h->stream;
+    // RLT1: iteration 0, then sb_iters x (spread + C pair mean,
+    // concentrate C->B, concentrate B->LB) for every candidate child at once
+    if ((e = launch_rlt1_init(h->node, R, h->dF, h->dDist, st)) ||
+        (e = launch_rlt1_lap(R, 1, 1, h->num_sms, st)) || (e = launch_rlt1_lap(R, 0, 0, h->num_sms, st)))
+        return cuda_fail(h, e, "rlt1");
+    for (int t = 0; t < sb_iters; t++)
+        if ((e = launch_rlt1_pair(R, st)) || (e = launch_rlt1_lap(R, 1, 0, h->num_sms, st)) ||
+            (e = launch_rlt1_lap(R, 0, 0, h->num_sms, st)))
+            return cuda_fail(h, e, "rlt1");
+    if ((e = cudaMemcpyAsync(h->h_lbd.data(), R.lbd, (size_t)R.K * 8, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaMemcpyAsync(h->h_kap.data(), R.kap, (size_t)R.K * 8, cudaMemcpyDeviceToHost, st)) ||
+        (e = cudaStreamSynchronize(st)))
+        return cuda_fail(h, e, "rlt1 result");
+    for (int c = 0; c < R.K; c++) est[c] = (double)h->h_kap[c] + h->h_lbd[c];
+    // max-min line selection (ties: lowest index, a row before a column)
+    double best = -INFINITY;
+    *kind = 0;
+    *index = 0;
+    for (int a2 = 0; a2 < n; a2++) {
+        double sc = INFINITY;
+        for (int b = 0; b < n; b++) sc = est[a2 * n + b] < sc ? est[a2 * n + b] : sc;
+        if (sc > best) {
+            best = sc;
+            *kind = 0;
+            *index = a2;
+        }
+    }
+    for (int b = 0; b < n; b++) {
+        double sc = INFINITY;
+        for (int a2 = 0; a2 < n; a2++) sc = est[a2 * n + b] < sc ? est[a2 * n + b] : sc;
+        if (sc > best) {
+            best = sc;
+            *kind = 1;
+            *index = b;
+        }
+    }
+    return QAP_OK;
+}
+
 qap_status qap_rlt2_dual_sizes(const qap_rlt2 *h, int64_t *nB, int64_t *nC, int64_t *nD)
 {
     if (!h) return QAP_E_ARG;
@@ -781,7 +869,8 @@ struct Bnb {
     bool have;
     int64_t best;
     std::vector<int32_t> best_perm;
-    int64_t bounded = 0, leaves = 0, pruned = 0;
+    int64_t bounded = 0, leaves = 0, pruned = 0, sb_cut = 0;
+    int sb_iters = -1;
     qap_status st = QAP_OK;
     const qap_rlt2 *h0() const { return pool[0]; }
 
@@ -833,49 +922,84 @@ struct Bnb {
         std::vector<char> used(floc.size(), 0);
         leaf_rec(perm, ffac, floc, 0, used);
     }
-    // bound the nodes (fac + {f -> x}) for x in xs, concurrently; LBs in the same order
-    bool bound_children(std::vector<int32_t> &fac, std::vector<int32_t> &loc, int f, const std::vector<int> &xs,
-                        std::vector<double> &lb)
+    // bound the children (fac + {fs[c] -> ls[c]}), `pool.size()` at a time concurrently
+    bool bound_children(std::vector<int32_t> &fac, std::vector<int32_t> &loc, const std::vector<int> &fs,
+                        const std::vector<int> &ls, const std::vector<char> &want, std::vector<double> &lb)
     {
-        lb.assign(xs.size(), 0.0);
+        lb.assign(fs.size(), INFINITY);
+        std::vector<size_t> idx;
+        for (size_t c = 0; c < fs.size(); c++)
+            if (want[c]) idx.push_back(c);
         const size_t B = pool.size();
-        for (size_t c0 = 0; c0 < xs.size(); c0 += B) {
-            const size_t c1 = c0 + B < xs.size() ? c0 + B : xs.size();
-            for (size_t c = c0; c < c1; c++) {
-                qap_rlt2 *h = pool[c - c0];
-                fac.push_back(f);
-                loc.push_back(xs[c]);
+        for (size_t c0 = 0; c0 < idx.size(); c0 += B) {
+            const size_t c1 = c0 + B < idx.size() ? c0 + B : idx.size();
+            for (size_t k = c0; k < c1; k++) {
+                qap_rlt2 *h = pool[k - c0];
+                fac.push_back(fs[idx[k]]);
+                loc.push_back(ls[idx[k]]);
                 st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data());
                 fac.pop_back();
                 loc.pop_back();
                 if (st != QAP_OK) return false;
                 if ((st = qap_rlt2_bound_async(h, iters, K, UB)) != QAP_OK) return false;
             }
-            for (size_t c = c0; c < c1; c++) {
+            for (size_t k = c0; k < c1; k++) {
                 qap_rlt2_result r{};
-                if ((st = qap_rlt2_bound_result(pool[c - c0], &r)) != QAP_OK) return false;
-                lb[c] = r.lb;
-                bounded++;
+                if ((st = qap_rlt2_bound_result(pool[k - c0], &r)) != QAP_OK) return false;
+                lb[idx[k]] = r.lb;
             }
         }
         return true;
     }
-    // node (fac, loc) is bounded and not pruned: expand it
+    // node (fac, loc) is bounded and not pruned: expand it.  Counters are taken when a
+    // child is reached in DFS order, with the incumbent of that moment (as the oracle).
     void expand(std::vector<int32_t> &fac, std::vector<int32_t> &loc)
     {
         if (st != QAP_OK) return;
         std::vector<int> ffac, floc;
         free_sets(fac, loc, ffac, floc);
-        const int f = ffac[0];
-        const bool child_leaf = ffac.size() - 1 <= 3;
+        const int n = (int)ffac.size();
+        std::vector<int> fs, ls;
+        std::vector<double> est;  // strong branching: RLT1 estimate of each child (else -inf)
+        if (sb_iters >= 0 && n >= 5) {
+            if ((st = qap_rlt2_fix(pool[0], (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return;
+            std::vector<double> e((size_t)n * n);
+            int32_t kind = 0, index = 0;
+            if ((st = qap_rlt2_strong_branch(pool[0], sb_iters, e.data(), &kind, &index)) != QAP_OK) return;
+            for (int x = 0; x < n; x++) {
+                const int a = kind == 0 ? index : x, b = kind == 0 ? x : index;
+                fs.push_back(ffac[a]);
+                ls.push_back(floc[b]);
+                est.push_back(e[(size_t)a * n + b]);
+            }
+        } else {
+            for (int x = 0; x < n; x++) {
+                fs.push_back(ffac[0]);
+                ls.push_back(floc[x]);
+                est.push_back(-INFINITY);
+            }
+        }
+        const bool child_leaf = n - 1 <= 3;
         std::vector<double> lb;
-        if (!child_leaf && !bound_children(fac, loc, f, floc, lb)) return;
-        for (size_t c = 0; c < floc.size(); c++) {
-            fac.push_back(f);
-            loc.push_back(floc[c]);
-            if (child_leaf) leaf(fac, loc);
-            else if (lb[c] > UB - 1.0 + 1e-6) pruned++;
-            else expand(fac, loc);
+        if (!child_leaf) {
+            std::vector<char> want(fs.size());
+            for (size_t c = 0; c < fs.size(); c++) want[c] = !(est[c] > UB - 1.0 + 1e-6);
+            if (!bound_children(fac, loc, fs, ls, want, lb)) return;
+        }
+        for (size_t c = 0; c < fs.size(); c++) {
+            if (est[c] > UB - 1.0 + 1e-6) {  // cut by its RLT1 estimate (strong branching)
+                sb_cut++;
+                continue;
+            }
+            fac.push_back(fs[c]);
+            loc.push_back(ls[c]);
+            if (child_leaf) {
+                leaf(fac, loc);
+            } else {
+                bounded++;
+                if (lb[c] > UB - 1.0 + 1e-6) pruned++;
+                else expand(fac, loc);
+            }
             fac.pop_back();
             loc.pop_back();
             if (st != QAP_OK) return;
@@ -906,8 +1030,9 @@ struct Bnb {
 };
 }  // namespace
 
-qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int64_t *opt, int32_t *perm,
-                         int64_t *bounded, int64_t *leaves, int64_t *pruned)
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int32_t sb_iters,
+                         int64_t *opt, int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned,
+                         int64_t *sb_cut)
 {
     if (!h || !opt || !perm || iters < 0) return QAP_E_ARG;
     if (h->world > 1 && batch > 1) return fail(h, QAP_E_ARG, "batched B&B needs a single-GPU handle");
@@ -919,6 +1044,7 @@ qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32
     b.UB = UB0;
     b.have = false;
     b.best = -1;
+    b.sb_iters = sb_iters;
     const int B = batch < 1 ? 1 : (batch > b.N ? b.N : batch);
     for (int k = 1; k < B; k++) {  // helper handles, each on its own stream
         cudaStream_t s = nullptr;
@@ -943,6 +1069,7 @@ qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32
     if (bounded) *bounded = b.bounded;
     if (leaves) *leaves = b.leaves;
     if (pruned) *pruned = b.pruned;
+    if (sb_cut) *sb_cut = b.sb_cut;
     return QAP_OK;
 }
 

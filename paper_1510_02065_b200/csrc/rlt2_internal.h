@@ -63,7 +63,8 @@ inline void make_geom(int n, Geom &g)
 }
 
 // LAP launch levels.
-enum LapLevel { LAP_L2 = 0, LAP_L1_ACC = 1, LAP_L1_SET = 2, LAP_L0_ITER0 = 3, LAP_L0 = 4, LAP_BATCH = 5 };
+enum LapLevel { LAP_L2 = 0, LAP_L1_ACC = 1, LAP_L1_SET = 2, LAP_L0_ITER0 = 3, LAP_L0 = 4, LAP_BATCH = 5,
+                LAP_L0_MULTI = 6 };
 
 struct LapBatchOut {
     double *R, *S, *u, *v;
@@ -72,7 +73,23 @@ struct LapBatchOut {
     int32_t *err;
 };
 
+// Batched RLT1 evaluation of the n^2 candidate children of a node (strong branching).
+struct Rlt1Batch {
+    int K;            // children (n * n)
+    Geom g;           // geometry of a child (n' = n - 1)
+    double *C;        // K * n'^2 blocks of stride g.ldc
+    double *B;        // K * bstr
+    int64_t bstr;     // even >= n'^2
+    double *lbd;      // K accumulated concentration sums
+    long long *kap;   // K fixed-fixed costs
+};
+
 // ---- launchers (rlt2_kernels.cu) -----------------------------------------------------
+cudaError_t launch_rlt1_init(const Node &parent, const Rlt1Batch &R, const int64_t *F, const int64_t *Dist,
+                             cudaStream_t st);
+cudaError_t launch_rlt1_pair(const Rlt1Batch &R, cudaStream_t st);
+// level 1 (acc: iteration 0) or level 0 LAPs of every child
+cudaError_t launch_rlt1_lap(const Rlt1Batch &R, int level1, int acc, int num_sms, cudaStream_t st);
 cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const int64_t *Dist,
                         double *B, double *C, int *triples, Ctl *ctl, cudaStream_t st);
 cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaStream_t st);

@@ -371,6 +371,8 @@ struct LapArgs {
     LapBatchOut bo;
     Sched *sched;  // non-null: dynamic queue + wait for the transfer of each block's facility
     int ntile3;    // transfer CTAs per facility triple
+    int64_t bdiv, bstr;  // level 1: B index of block b = (b / bdiv) * bstr + b % bdiv (batched RLT1)
+    double *lbm;         // LAP_L0_MULTI: lbm[b] += S
 };
 
 // First (canonical) facility of stored block b; `hint` only moves forward.
@@ -504,8 +506,14 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
                 a.C[(int64_t)(k * n + l) * g.ldc + i * n1 + (j - (j > l))] = S;
                 break;
             }
-            case LAP_L1_ACC: a.B[b] = a.B[b] + S; break;
-            case LAP_L1_SET: a.B[b] = S; break;  // B was spread and zeroed: 0 + S = S
+            case LAP_L1_ACC:
+            case LAP_L1_SET: {
+                const int64_t bi = a.bdiv ? (b / a.bdiv) * a.bstr + b % a.bdiv : b;
+                if (a.lvl == LAP_L1_ACC) a.B[bi] = a.B[bi] + S;
+                else a.B[bi] = S;  // B was spread and zeroed: 0 + S = S
+                break;
+            }
+            case LAP_L0_MULTI: a.lbm[b] = a.lbm[b] + S; break;
             case LAP_L0_ITER0:
             case LAP_L0: {
                 Ctl *c = a.ctl;
@@ -805,6 +813,78 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Strong branching: RLT1 bounds of the n^2 candidate children of a node at once.
+// Child c = a * n + b fixes free facility I[a] at free location J[b] in addition to the
+// node's pairs; its reduced costs are built as in k_init (O0/O1).
+// ---------------------------------------------------------------------------------------
+__global__ void k_rlt1_init(const Node nd, const Rlt1Batch R, const int64_t *__restrict__ F,
+                            const int64_t *__restrict__ Dist)
+{
+    const int N = nd.N, n = nd.n, c = blockIdx.y, ca = c / n, cb = c - ca * n;
+    const int np = n - 1, np1 = np - 1;  // child size n', n'-1
+    const int fa = nd.I[ca], la = nd.J[cb];
+    const int64_t n4 = (int64_t)np * np * np * np;
+    const int64_t tot = n4 + (int64_t)np * np;
+    double *C = R.C + (int64_t)c * np * np * R.g.ldc;
+    double *B = R.B + (int64_t)c * R.bstr;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+        if (x < n4) {
+            const int l = (int)(x % np), k = (int)((x / np) % np), j = (int)((x / np / np) % np),
+                      i = (int)(x / np / np / np);
+            if (k == i || l == j) continue;
+            const int Ii = nd.I[i + (i >= ca)], Ik = nd.I[k + (k >= ca)];
+            const int Jj = nd.J[j + (j >= cb)], Jl = nd.J[l + (l >= cb)];
+            C[(int64_t)(i * np + j) * R.g.ldc + (k - (k > i)) * np1 + (l - (l > j))] =
+                (double)(F[Ii * N + Ik] * Dist[Jj * N + Jl]);
+        } else {
+            const int y = (int)(x - n4), a_ = y / np, b_ = y % np;
+            const int Ia = nd.I[a_ + (a_ >= ca)], Jb = nd.J[b_ + (b_ >= cb)];
+            int64_t v = F[Ia * N + Ia] * Dist[Jb * N + Jb];
+            for (int t = 0; t < nd.m; t++)
+                v += F[nd.fac[t] * N + Ia] * Dist[nd.loc[t] * N + Jb] + F[Ia * N + nd.fac[t]] * Dist[Jb * N + nd.loc[t]];
+            v += F[fa * N + Ia] * Dist[la * N + Jb] + F[Ia * N + fa] * Dist[Jb * N + la];
+            B[y] = (double)v;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // kappa: fixed-fixed cost incl. the new pair
+        long long kap = 0;
+        for (int t = 0; t <= nd.m; t++) {
+            const int f1 = t < nd.m ? nd.fac[t] : fa, l1 = t < nd.m ? nd.loc[t] : la;
+            for (int t2 = 0; t2 <= nd.m; t2++) {
+                const int f2 = t2 < nd.m ? nd.fac[t2] : fa, l2 = t2 < nd.m ? nd.loc[t2] : la;
+                kap += F[f1 * N + f2] * Dist[l1 * N + l2];
+            }
+        }
+        R.kap[c] = kap;
+        R.lbd[c] = 0.0;
+    }
+}
+
+// RLT1 iteration, first half (P:216 spread B->C, then P:189 transfer between the
+// complementary costs of C = pair mean, reading R13):
+//   a = c_ij[kl] + b_ij/(n'-1), b = c_kl[ij] + b_kl/(n'-1), both <- (a + b) / 2.
+__global__ void k_rlt1_pair(const Rlt1Batch R)
+{
+    const int np = R.g.n, np1 = np - 1;
+    const int64_t n4 = (int64_t)np * np * np * np;
+    const double div1 = (double)(np - 1);
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n4 * R.K; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = x / n4, y = x - c * n4;
+        const int l = (int)(y % np), k = (int)((y / np) % np), j = (int)((y / np / np) % np), i = (int)(y / np / np / np);
+        if (k <= i || l == j) continue;
+        double *C = R.C + c * np * np * R.g.ldc;
+        const double *B = R.B + c * R.bstr;
+        double *p1 = C + (int64_t)(i * np + j) * R.g.ldc + (k - 1) * np1 + (l - (l > j));
+        double *p2 = C + (int64_t)(k * np + l) * R.g.ldc + i * np1 + (j - (j > l));
+        const double a = *p1 + B[i * np + j] / div1;
+        const double b = *p2 + B[k * np + l] / div1;
+        const double mu = (a + b) / 2.0;
+        *p1 = mu;
+        *p2 = mu;
+    }
+}
+
 // Sharded iteration: level-2 values S of every stored block (all-gathered, global block
 // order) credited to both complementary coefficients (reading R12), on every rank.
 __global__ void k_credit(const Geom g, const double *__restrict__ S, const Offsets pos, double *__restrict__ C,
@@ -965,6 +1045,52 @@ cudaError_t launch_lap_l2_local(const Geom &g, double *Dloc, int64_t count, doub
     a.sched = sched;  // dynamic queue (reset by k_sigma), no transfer waits
     a.ntile3 = 0;
     return dispatch_lap(a, num_sms, lap_cfg, st);
+}
+
+cudaError_t launch_rlt1_init(const Node &parent, const Rlt1Batch &R, const int64_t *F, const int64_t *Dist,
+                             cudaStream_t st)
+{
+    const int np = R.g.n;
+    const int64_t tot = (int64_t)np * np * np * np + (int64_t)np * np;
+    int bx = (int)((tot + 255) / 256);
+    if (bx > 64) bx = 64;
+    dim3 grid(bx, R.K);
+    k_rlt1_init<<<grid, 256, 0, st>>>(parent, R, F, Dist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rlt1_pair(const Rlt1Batch &R, cudaStream_t st)
+{
+    const int64_t tot = (int64_t)R.g.n * R.g.n * R.g.n * R.g.n * R.K;
+    int blocks = (int)((tot + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_rlt1_pair<<<blocks, 256, 0, st>>>(R);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rlt1_lap(const Rlt1Batch &R, int level1, int acc, int num_sms, cudaStream_t st)
+{
+    LapArgs a{};
+    a.g = R.g;
+    const int np = R.g.n;
+    if (level1) {
+        a.lvl = acc ? LAP_L1_ACC : LAP_L1_SET;
+        a.m = np - 1;
+        a.count = (int64_t)R.K * np * np;
+        a.ld = R.g.ldc;
+        a.src = a.dst = R.C;
+        a.B = R.B;
+        a.bdiv = (int64_t)np * np;
+        a.bstr = R.bstr;
+        return dispatch_lap(a, num_sms, 8, st);
+    }
+    a.lvl = LAP_L0_MULTI;
+    a.m = np;
+    a.count = R.K;
+    a.ld = R.bstr;
+    a.src = a.dst = R.B;
+    a.lbm = R.lbd;
+    return dispatch_lap(a, num_sms, 4, st);
 }
 
 cudaError_t launch_lap_batch(int m, int64_t count, int64_t ld, const double *M, const LapBatchOut &o, int num_sms,

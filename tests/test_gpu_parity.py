@@ -320,3 +320,29 @@ def test_bound_async_concurrent(torch, pkg):
         pkg.qap_rlt2_fix(h, fx)
         assert pkg.qap_rlt2_bound(h, 4)["lb"] == r["lb"]
         pkg.qap_destroy(h)
+
+
+@pytest.mark.parametrize("family,n,fixed", [("taib", 7, ()), ("nug", 9, ((1, 2),)), ("uniform", 12, ((0, 5), (3, 3)))])
+def test_strong_branch_vs_oracle(orc, torch, pkg, family, n, fixed):
+    """NEXT-1: RLT1 estimates of every candidate child and the selected line."""
+    inst = qapgen.make(family, n, 2)
+    h = pkg.qap_rlt2_create(n, inst.F, inst.D)
+    pkg.qap_rlt2_fix(h, fixed)
+    est, kind, index = pkg.qap_rlt2_strong_branch(h, 2)
+    oest, okind, oindex = orc.strong_branch(inst.F, inst.D, fixed, T=2)
+    rel_close(est, oest)
+    assert (est == oest).all()
+    assert (kind, index) == (okind, oindex)
+    pkg.qap_destroy(h)
+
+
+@pytest.mark.parametrize("batch", [1, 8])
+@pytest.mark.parametrize("family,n", [("nug", 8), ("taib", 9), ("uniform", 8)])
+def test_bnb_strong_branching_parity(orc, torch, pkg, family, n, batch):
+    inst = qapgen.make(family, n, 1)
+    h = pkg.qap_rlt2_create(n, inst.F, inst.D)
+    g = pkg.qap_bnb_solve(h, 2, batch=batch, sb_iters=1)
+    o = orc.bnb(inst.F, inst.D, T=2, sb_iters=1)
+    assert g["opt"] == o["opt"] and (g["perm"] == o["perm"]).all()
+    assert (g["bounded"], g["leaves"], g["pruned"], g["sb_cut"]) == (o["bounded"], o["leaves"], o["pruned"], o["sb_cut"])
+    pkg.qap_destroy(h)
