@@ -250,6 +250,34 @@ qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32
                          int64_t *sb_cut);
 
 /*
+ * qap_bnb_run — qap_bnb_solve with checkpoint / resume (interruptions of multi-day
+ *   solves).  The search state (stack of expanded nodes with their
+ *   children's bounds, incumbent, counters) is written atomically (<path>.tmp + rename) to
+ *   checkpoint_path every checkpoint_every bounded nodes and when the run stops early
+ *   (max_nodes > 0: at most that many nodes bounded by this call).  resume != 0 continues
+ *   from checkpoint_path (same instance and parameters, checked by digest); a resumed run
+ *   makes exactly the decisions of an uninterrupted one.  out->complete = 1 when the tree
+ *   is exhausted.
+ */
+typedef struct {
+    int32_t iters;            /* RLT2 iterations per node                               */
+    double K, UB0;            /* stop parameter, initial upper bound (+INFINITY: none)  */
+    int32_t batch;            /* children bounded concurrently                          */
+    int32_t sb_iters;         /* >= 0: strong branching with RLT1, else off             */
+    const char *checkpoint_path;
+    int64_t checkpoint_every; /* bounded nodes between checkpoints (0: only on stop)    */
+    int64_t max_nodes;        /* stop after this many bounded nodes (0: no limit)       */
+    int32_t resume;
+} qap_bnb_opts;
+typedef struct {
+    int64_t opt;              /* best objective found (-1: none better than UB0)        */
+    int32_t perm[64];
+    int64_t bounded, leaves, pruned, sb_cut;
+    int32_t complete;
+} qap_bnb_result;
+qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *opts, qap_bnb_result *out);
+
+/*
  * qap_rlt2_strong_branch — strong branching with the RLT1 dual: every candidate
  *   child of the handle's current node (free facility I[a] at free location J[b], reduced
  *   indices, n = free facilities >= 4) is bounded by a cold RLT1 ascent (Algorithm 1 without

@@ -33,7 +33,18 @@ EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
            "qap_destroy", "qap_lap_batch", "qap_bnb_solve", "qap_nccl_unique_id", "qap_rlt2_shard_info",
            "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound", "qap_rlt2_bound_async",
-           "qap_rlt2_bound_result", "qap_rlt2_strong_branch"]
+           "qap_rlt2_bound_result", "qap_rlt2_strong_branch", "qap_bnb_run"]
+
+
+class _BnbOpts(ct.Structure):
+    _fields_ = [("iters", ct.c_int32), ("K", ct.c_double), ("UB0", ct.c_double), ("batch", ct.c_int32),
+                ("sb_iters", ct.c_int32), ("checkpoint_path", ct.c_char_p), ("checkpoint_every", ct.c_int64),
+                ("max_nodes", ct.c_int64), ("resume", ct.c_int32)]
+
+
+class _BnbResult(ct.Structure):
+    _fields_ = [("opt", ct.c_int64), ("perm", ct.c_int32 * 64), ("bounded", ct.c_int64), ("leaves", ct.c_int64),
+                ("pruned", ct.c_int64), ("sb_cut", ct.c_int64), ("complete", ct.c_int32)]
 
 
 class QapError(RuntimeError):
@@ -83,6 +94,7 @@ def load_library(path: str = LIB_PATH):
     L.qap_bnb_solve.argtypes = [vp, i32, f64, f64, i32, i32, ct.POINTER(i64), vp, ct.POINTER(i64),
                                 ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
     L.qap_rlt2_strong_branch.argtypes = [vp, i32, vp, ct.POINTER(i32), ct.POINTER(i32)]
+    L.qap_bnb_run.argtypes = [vp, ct.POINTER(_BnbOpts), ct.POINTER(_BnbResult)]
     L.qap_rlt2_bound_async.argtypes = [vp, i32, f64, f64]
     L.qap_rlt2_bound_result.argtypes = [vp, ct.POINTER(_Result)]
     L.qap_nccl_unique_id.argtypes = [vp]
@@ -253,6 +265,18 @@ def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, 
     _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, batch, sb_iters, ct.byref(opt), perm.ctypes.data,
                                         ct.byref(b), ct.byref(l), ct.byref(p), ct.byref(c)), h)
     return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
+
+
+def qap_bnb_run(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
+                sb_iters: int = -1, checkpoint_path: str | None = None, checkpoint_every: int = 0,
+                max_nodes: int = 0, resume: bool = False) -> dict:
+    """B&B with checkpoint/resume (see include/qap_rlt2.h)."""
+    o = _BnbOpts(iters, K, UB0, batch, sb_iters, checkpoint_path.encode() if checkpoint_path else None,
+                 checkpoint_every, max_nodes, int(resume))
+    r = _BnbResult()
+    _check(load_library().qap_bnb_run(h.ptr, ct.byref(o), ct.byref(r)), h)
+    return dict(opt=r.opt, perm=np.array(r.perm[: h.N], np.int32), bounded=r.bounded, leaves=r.leaves,
+                pruned=r.pruned, sb_cut=r.sb_cut, complete=bool(r.complete))
 
 
 def qap_rlt2_strong_branch(h: Handle, sb_iters: int = 1):

@@ -852,25 +852,37 @@ qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_d
     return QAP_OK;
 }
 
+}  // extern "C"
+
 // ---- minimal deterministic B&B (P:236-238 caller) ----------------------
-// Depth-first; a node is bounded when its parent is expanded: the children of a node are
-// bounded together, `batch` at a time, each on its own handle and stream (independent
-// subproblems run concurrently on the GPU).  Children are then visited in ascending
-// location order and pruned against the CURRENT incumbent.  With K = 0 this makes exactly
-// the decisions of the one-node-at-a-time DFS (a bound only stops early when LB already
-// exceeds UB - 1 + 1e-6, and LB is nondecreasing), so node counts, optimum and
-// permutation equal the oracle's sequential B&B.
+// Depth-first over an explicit stack of frames.  A frame is an expanded node: its children
+// (branching line), their RLT1 estimates (strong branching) and RLT2 bounds, and the next
+// child to visit.  Children of a node are bounded together, `batch` at a time, each on its
+// own handle and stream; they are then visited in order and pruned against the CURRENT
+// incumbent.  With K = 0 this makes exactly the decisions of the one-node-at-a-time DFS
+// (a bound stops early only when LB already exceeds UB - 1 + 1e-6, and LB is
+// nondecreasing), so node counts, optimum and permutation equal the oracle's B&B.
+// The stack + incumbent + counters are the checkpoint ("checkpoints procedure").
 namespace {
+struct Frame {
+    std::vector<int32_t> fac, loc;  // the expanded node
+    std::vector<int32_t> fs, ls;    // its children: fac + fs[c] -> loc + ls[c]
+    std::vector<double> est, lb;    // RLT1 estimate (-inf without strong branching), RLT2 bound
+    uint32_t next = 0;
+    uint8_t child_leaf = 0;
+};
+
 struct Bnb {
     std::vector<qap_rlt2 *> pool;  // pool[0] = the caller's handle
     std::vector<cudaStream_t> own_streams;
-    int N, iters;
-    double K, UB;
-    bool have;
-    int64_t best;
+    int N = 0, iters = 0, sb_iters = -1;
+    double K = 0.0, UB = INFINITY, UB0 = INFINITY;
+    bool have = false;
+    int64_t best = -1;
     std::vector<int32_t> best_perm;
     int64_t bounded = 0, leaves = 0, pruned = 0, sb_cut = 0;
-    int sb_iters = -1;
+    std::vector<Frame> stack;
+    bool root_done = false;
     qap_status st = QAP_OK;
     const qap_rlt2 *h0() const { return pool[0]; }
 
@@ -922,21 +934,21 @@ struct Bnb {
         std::vector<char> used(floc.size(), 0);
         leaf_rec(perm, ffac, floc, 0, used);
     }
-    // bound the children (fac + {fs[c] -> ls[c]}), `pool.size()` at a time concurrently
-    bool bound_children(std::vector<int32_t> &fac, std::vector<int32_t> &loc, const std::vector<int> &fs,
-                        const std::vector<int> &ls, const std::vector<char> &want, std::vector<double> &lb)
+    // bound the wanted children of F, `pool.size()` at a time concurrently
+    bool bound_children(Frame &F, const std::vector<char> &want)
     {
-        lb.assign(fs.size(), INFINITY);
+        F.lb.assign(F.fs.size(), INFINITY);
         std::vector<size_t> idx;
-        for (size_t c = 0; c < fs.size(); c++)
+        for (size_t c = 0; c < F.fs.size(); c++)
             if (want[c]) idx.push_back(c);
         const size_t B = pool.size();
+        std::vector<int32_t> fac = F.fac, loc = F.loc;
         for (size_t c0 = 0; c0 < idx.size(); c0 += B) {
             const size_t c1 = c0 + B < idx.size() ? c0 + B : idx.size();
             for (size_t k = c0; k < c1; k++) {
                 qap_rlt2 *h = pool[k - c0];
-                fac.push_back(fs[idx[k]]);
-                loc.push_back(ls[idx[k]]);
+                fac.push_back(F.fs[idx[k]]);
+                loc.push_back(F.ls[idx[k]]);
                 st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data());
                 fac.pop_back();
                 loc.pop_back();
@@ -946,68 +958,50 @@ struct Bnb {
             for (size_t k = c0; k < c1; k++) {
                 qap_rlt2_result r{};
                 if ((st = qap_rlt2_bound_result(pool[k - c0], &r)) != QAP_OK) return false;
-                lb[idx[k]] = r.lb;
+                F.lb[idx[k]] = r.lb;
             }
         }
         return true;
     }
-    // node (fac, loc) is bounded and not pruned: expand it.  Counters are taken when a
-    // child is reached in DFS order, with the incumbent of that moment (as the oracle).
-    void expand(std::vector<int32_t> &fac, std::vector<int32_t> &loc)
+    // node (fac, loc) is bounded and not pruned: its frame (branching line + child bounds)
+    bool make_frame(const std::vector<int32_t> &fac, const std::vector<int32_t> &loc, Frame &F)
     {
-        if (st != QAP_OK) return;
+        F.fac = fac;
+        F.loc = loc;
         std::vector<int> ffac, floc;
         free_sets(fac, loc, ffac, floc);
         const int n = (int)ffac.size();
-        std::vector<int> fs, ls;
-        std::vector<double> est;  // strong branching: RLT1 estimate of each child (else -inf)
-        if (sb_iters >= 0 && n >= 5) {
-            if ((st = qap_rlt2_fix(pool[0], (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return;
+        if (sb_iters >= 0 && n >= 5) {  // strong branching
+            if ((st = qap_rlt2_fix(pool[0], (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return false;
             std::vector<double> e((size_t)n * n);
             int32_t kind = 0, index = 0;
-            if ((st = qap_rlt2_strong_branch(pool[0], sb_iters, e.data(), &kind, &index)) != QAP_OK) return;
+            if ((st = qap_rlt2_strong_branch(pool[0], sb_iters, e.data(), &kind, &index)) != QAP_OK) return false;
             for (int x = 0; x < n; x++) {
                 const int a = kind == 0 ? index : x, b = kind == 0 ? x : index;
-                fs.push_back(ffac[a]);
-                ls.push_back(floc[b]);
-                est.push_back(e[(size_t)a * n + b]);
+                F.fs.push_back(ffac[a]);
+                F.ls.push_back(floc[b]);
+                F.est.push_back(e[(size_t)a * n + b]);
             }
-        } else {
+        } else {  // lowest free facility, locations ascending (R20)
             for (int x = 0; x < n; x++) {
-                fs.push_back(ffac[0]);
-                ls.push_back(floc[x]);
-                est.push_back(-INFINITY);
+                F.fs.push_back(ffac[0]);
+                F.ls.push_back(floc[x]);
+                F.est.push_back(-INFINITY);
             }
         }
-        const bool child_leaf = n - 1 <= 3;
-        std::vector<double> lb;
-        if (!child_leaf) {
-            std::vector<char> want(fs.size());
-            for (size_t c = 0; c < fs.size(); c++) want[c] = !(est[c] > UB - 1.0 + 1e-6);
-            if (!bound_children(fac, loc, fs, ls, want, lb)) return;
+        F.child_leaf = n - 1 <= 3;
+        if (F.child_leaf) {
+            F.lb.assign(F.fs.size(), -INFINITY);
+            return true;
         }
-        for (size_t c = 0; c < fs.size(); c++) {
-            if (est[c] > UB - 1.0 + 1e-6) {  // cut by its RLT1 estimate (strong branching)
-                sb_cut++;
-                continue;
-            }
-            fac.push_back(fs[c]);
-            loc.push_back(ls[c]);
-            if (child_leaf) {
-                leaf(fac, loc);
-            } else {
-                bounded++;
-                if (lb[c] > UB - 1.0 + 1e-6) pruned++;
-                else expand(fac, loc);
-            }
-            fac.pop_back();
-            loc.pop_back();
-            if (st != QAP_OK) return;
-        }
+        std::vector<char> want(F.fs.size());
+        for (size_t c = 0; c < F.fs.size(); c++) want[c] = !(F.est[c] > UB - 1.0 + 1e-6);
+        return bound_children(F, want);
     }
-    void run()
+    void start()
     {
         std::vector<int32_t> fac, loc;
+        root_done = true;
         if (N <= 3) {
             leaf(fac, loc);
             return;
@@ -1020,7 +1014,37 @@ struct Bnb {
             pruned++;
             return;
         }
-        expand(fac, loc);
+        Frame F;
+        if (!make_frame(fac, loc, F)) return;
+        stack.push_back(std::move(F));
+    }
+    // advance by one child; false when the search is over
+    bool step()
+    {
+        while (!stack.empty() && stack.back().next >= stack.back().fs.size()) stack.pop_back();
+        if (stack.empty()) return false;
+        Frame &T = stack.back();
+        const uint32_t c = T.next++;
+        if (T.est[c] > UB - 1.0 + 1e-6) {  // cut by its RLT1 estimate (strong branching)
+            sb_cut++;
+            return true;
+        }
+        std::vector<int32_t> fac = T.fac, loc = T.loc;
+        fac.push_back(T.fs[c]);
+        loc.push_back(T.ls[c]);
+        if (T.child_leaf) {
+            leaf(fac, loc);
+            return true;
+        }
+        bounded++;
+        if (T.lb[c] > UB - 1.0 + 1e-6) {
+            pruned++;
+            return true;
+        }
+        Frame F;
+        if (!make_frame(fac, loc, F)) return false;
+        stack.push_back(std::move(F));
+        return true;
     }
     ~Bnb()
     {
@@ -1028,48 +1052,253 @@ struct Bnb {
         for (auto s : own_streams) cudaStreamDestroy(s);
     }
 };
+
+// ---- checkpoint file (binary, little-endian; written to <path>.tmp then renamed) --------
+constexpr uint64_t kCkptMagic = 0x3154504b32544c52ull;  // "RLT2KPT1"
+
+uint64_t instance_digest(const qap_rlt2 *h)
+{
+    uint64_t x = 1469598103934665603ull;  // FNV-1a over N, F, D
+    auto mix = [&](uint64_t v) {
+        for (int b = 0; b < 8; b++) {
+            x ^= (v >> (8 * b)) & 0xff;
+            x *= 1099511628211ull;
+        }
+    };
+    mix((uint64_t)h->N);
+    for (auto v : h->F) mix((uint64_t)v);
+    for (auto v : h->Dist) mix((uint64_t)v);
+    return x;
+}
+
+template <class T>
+void put(std::vector<char> &o, const T &v)
+{
+    const char *p = reinterpret_cast<const char *>(&v);
+    o.insert(o.end(), p, p + sizeof(T));
+}
+template <class T>
+void putv(std::vector<char> &o, const std::vector<T> &v)
+{
+    put(o, (uint64_t)v.size());
+    const char *p = reinterpret_cast<const char *>(v.data());
+    o.insert(o.end(), p, p + v.size() * sizeof(T));
+}
+struct Reader {
+    const std::vector<char> &b;
+    size_t pos = 0;
+    bool ok = true;
+    template <class T>
+    T get()
+    {
+        T v{};
+        if (pos + sizeof(T) > b.size()) {
+            ok = false;
+            return v;
+        }
+        memcpy(&v, b.data() + pos, sizeof(T));
+        pos += sizeof(T);
+        return v;
+    }
+    template <class T>
+    std::vector<T> getv()
+    {
+        const uint64_t n = get<uint64_t>();
+        std::vector<T> v;
+        if (!ok || n > (1ull << 32) || pos + n * sizeof(T) > b.size()) {
+            ok = false;
+            return v;
+        }
+        v.resize(n);
+        memcpy(v.data(), b.data() + pos, n * sizeof(T));
+        pos += n * sizeof(T);
+        return v;
+    }
+};
+
+bool save_checkpoint(const Bnb &B, const char *path, std::string &err)
+{
+    std::vector<char> o;
+    put(o, kCkptMagic);
+    put(o, instance_digest(B.h0()));
+    put(o, (int32_t)B.N);
+    put(o, (int32_t)B.iters);
+    put(o, (int32_t)B.sb_iters);
+    put(o, B.K);
+    put(o, B.UB0);
+    put(o, B.UB);
+    put(o, (uint8_t)B.have);
+    put(o, B.best);
+    putv(o, B.best_perm);
+    put(o, B.bounded);
+    put(o, B.leaves);
+    put(o, B.pruned);
+    put(o, B.sb_cut);
+    put(o, (uint64_t)B.stack.size());
+    for (const Frame &F : B.stack) {
+        putv(o, F.fac);
+        putv(o, F.loc);
+        putv(o, F.fs);
+        putv(o, F.ls);
+        putv(o, F.est);
+        putv(o, F.lb);
+        put(o, F.next);
+        put(o, F.child_leaf);
+    }
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) {
+        err = "cannot open " + tmp;
+        return false;
+    }
+    const bool wrote = fwrite(o.data(), 1, o.size(), f) == o.size() && fflush(f) == 0;
+    fclose(f);
+    if (!wrote || rename(tmp.c_str(), path) != 0) {
+        err = "cannot write checkpoint " + std::string(path);
+        return false;
+    }
+    return true;
+}
+
+bool load_checkpoint(Bnb &B, const char *path, std::string &err)
+{
+    FILE *f = fopen(path, "rb");
+    if (!f) {
+        err = "cannot open " + std::string(path);
+        return false;
+    }
+    std::vector<char> buf;
+    char tmp[1 << 16];
+    size_t r;
+    while ((r = fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + r);
+    fclose(f);
+    Reader R{buf};
+    if (R.get<uint64_t>() != kCkptMagic) {
+        err = "not a checkpoint file";
+        return false;
+    }
+    if (R.get<uint64_t>() != instance_digest(B.h0()) || R.get<int32_t>() != B.N || R.get<int32_t>() != B.iters ||
+        R.get<int32_t>() != B.sb_iters || R.get<double>() != B.K || R.get<double>() != B.UB0) {
+        err = "checkpoint belongs to another instance or parameters";
+        return false;
+    }
+    B.UB = R.get<double>();
+    B.have = R.get<uint8_t>() != 0;
+    B.best = R.get<int64_t>();
+    B.best_perm = R.getv<int32_t>();
+    B.bounded = R.get<int64_t>();
+    B.leaves = R.get<int64_t>();
+    B.pruned = R.get<int64_t>();
+    B.sb_cut = R.get<int64_t>();
+    const uint64_t nf = R.get<uint64_t>();
+    B.stack.clear();
+    for (uint64_t k = 0; k < nf && R.ok; k++) {
+        Frame F;
+        F.fac = R.getv<int32_t>();
+        F.loc = R.getv<int32_t>();
+        F.fs = R.getv<int32_t>();
+        F.ls = R.getv<int32_t>();
+        F.est = R.getv<double>();
+        F.lb = R.getv<double>();
+        F.next = R.get<uint32_t>();
+        F.child_leaf = R.get<uint8_t>();
+        B.stack.push_back(std::move(F));
+    }
+    if (!R.ok) {
+        err = "truncated checkpoint";
+        return false;
+    }
+    B.root_done = true;
+    return true;
+}
 }  // namespace
 
-qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int32_t sb_iters,
-                         int64_t *opt, int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned,
-                         int64_t *sb_cut)
+extern "C" {
+
+qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
 {
-    if (!h || !opt || !perm || iters < 0) return QAP_E_ARG;
-    if (h->world > 1 && batch > 1) return fail(h, QAP_E_ARG, "batched B&B needs a single-GPU handle");
+    if (!h || !o || !out || o->iters < 0) return QAP_E_ARG;
+    if (h->world > 1 && o->batch > 1) return fail(h, QAP_E_ARG, "batched B&B needs a single-GPU handle");
+    if ((o->resume || o->checkpoint_every > 0) && !o->checkpoint_path)
+        return fail(h, QAP_E_ARG, "checkpointing needs checkpoint_path");
     Bnb b;
     b.pool.push_back(h);
     b.N = h->N;
-    b.iters = iters;
-    b.K = K;
-    b.UB = UB0;
-    b.have = false;
-    b.best = -1;
-    b.sb_iters = sb_iters;
-    const int B = batch < 1 ? 1 : (batch > b.N ? b.N : batch);
+    b.iters = o->iters;
+    b.K = o->K;
+    b.UB = b.UB0 = o->UB0;
+    b.sb_iters = o->sb_iters;
+    const int B = o->batch < 1 ? 1 : (o->batch > b.N ? b.N : o->batch);
     for (int k = 1; k < B; k++) {  // helper handles, each on its own stream
         cudaStream_t s = nullptr;
         cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_fail(h, e, "bnb stream");
         b.own_streams.push_back(s);
-        qap_rlt2_opts o{};
-        o.device = h->device;
-        o.cuda_stream = s;
-        o.flags = h->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP);
-        o.lap_warps = h->lap_warps;
+        qap_rlt2_opts op{};
+        op.device = h->device;
+        op.cuda_stream = s;
+        op.flags = h->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP);
+        op.lap_warps = h->lap_warps;
         qap_rlt2 *x = nullptr;
-        qap_status st = qap_rlt2_create(h->N, h->F.data(), h->Dist.data(), &o, &x);
+        qap_status st = qap_rlt2_create(h->N, h->F.data(), h->Dist.data(), &op, &x);
         if (st != QAP_OK) return fail(h, st, std::string("bnb helper handle: ") + qap_last_error(nullptr));
         b.pool.push_back(x);
     }
-    b.run();
+    std::string err;
+    if (o->resume) {
+        if (!load_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
+    } else {
+        b.start();
+        if (b.st != QAP_OK) return b.st;
+    }
+    int64_t since = 0;
+    bool done = false;
+    const int64_t b0 = b.bounded;
+    while (true) {
+        if (o->max_nodes > 0 && b.bounded - b0 >= o->max_nodes) break;  // budget: stop here
+        const int64_t before = b.bounded;
+        if (!b.step()) {
+            done = b.st == QAP_OK;
+            break;
+        }
+        if (o->checkpoint_every > 0 && (since += b.bounded - before) >= o->checkpoint_every) {
+            since = 0;
+            if (!save_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
+        }
+    }
     if (b.st != QAP_OK) return b.st;
-    *opt = b.have ? b.best : -1;
-    if (b.have)
-        for (int x = 0; x < b.N; x++) perm[x] = b.best_perm[x];
-    if (bounded) *bounded = b.bounded;
-    if (leaves) *leaves = b.leaves;
-    if (pruned) *pruned = b.pruned;
-    if (sb_cut) *sb_cut = b.sb_cut;
+    if (!done && o->checkpoint_path && !save_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
+    out->complete = done ? 1 : 0;
+    out->opt = b.have ? b.best : -1;
+    for (int x = 0; x < b.N && x < 64; x++) out->perm[x] = b.have ? b.best_perm[x] : -1;
+    out->bounded = b.bounded;
+    out->leaves = b.leaves;
+    out->pruned = b.pruned;
+    out->sb_cut = b.sb_cut;
+    return QAP_OK;
+}
+
+qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32_t batch, int32_t sb_iters,
+                         int64_t *opt, int32_t *perm, int64_t *bounded, int64_t *leaves, int64_t *pruned,
+                         int64_t *sb_cut)
+{
+    if (!h || !opt || !perm) return QAP_E_ARG;
+    qap_bnb_opts o{};
+    o.iters = iters;
+    o.K = K;
+    o.UB0 = UB0;
+    o.batch = batch;
+    o.sb_iters = sb_iters;
+    qap_bnb_result r{};
+    qap_status s = qap_bnb_run(h, &o, &r);
+    if (s != QAP_OK) return s;
+    *opt = r.opt;
+    if (r.opt >= 0)
+        for (int x = 0; x < h->N; x++) perm[x] = r.perm[x];
+    if (bounded) *bounded = r.bounded;
+    if (leaves) *leaves = r.leaves;
+    if (pruned) *pruned = r.pruned;
+    if (sb_cut) *sb_cut = r.sb_cut;
     return QAP_OK;
 }
 

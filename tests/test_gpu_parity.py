@@ -346,3 +346,37 @@ def test_bnb_strong_branching_parity(orc, torch, pkg, family, n, batch):
     assert g["opt"] == o["opt"] and (g["perm"] == o["perm"]).all()
     assert (g["bounded"], g["leaves"], g["pruned"], g["sb_cut"]) == (o["bounded"], o["leaves"], o["pruned"], o["sb_cut"])
     pkg.qap_destroy(h)
+
+
+@pytest.mark.parametrize("sb", [-1, 1])
+def test_bnb_checkpoint_resume(orc, torch, pkg, tmp_path, sb):
+    """NEXT-4: stopping after a node budget and resuming from the checkpoint —
+    repeatedly, and from a periodic mid-run checkpoint — gives exactly the uninterrupted
+    result (node counts, optimum, permutation)."""
+    inst = qapgen.taib(9, 4)
+    h = pkg.qap_rlt2_create(9, inst.F, inst.D)
+    ref = pkg.qap_bnb_run(h, 2, batch=4, sb_iters=sb)
+    assert ref["complete"]
+    path = str(tmp_path / "bnb.ckpt")
+    r = pkg.qap_bnb_run(h, 2, batch=4, sb_iters=sb, checkpoint_path=path, max_nodes=7)
+    assert not r["complete"]
+    rounds = 0
+    while not r["complete"]:
+        r = pkg.qap_bnb_run(h, 2, batch=3, sb_iters=sb, checkpoint_path=path, max_nodes=5, resume=True)
+        rounds += 1
+        assert rounds < 1000
+    keys = ("opt", "bounded", "leaves", "pruned", "sb_cut")
+    assert all(r[k] == ref[k] for k in keys) and (r["perm"] == ref["perm"]).all()
+    # periodic checkpoints of a complete run: resuming from the last one finishes identically
+    full = pkg.qap_bnb_run(h, 2, batch=2, sb_iters=sb, checkpoint_path=path, checkpoint_every=3)
+    assert full["complete"] and all(full[k] == ref[k] for k in keys)
+    again = pkg.qap_bnb_run(h, 2, batch=2, sb_iters=sb, checkpoint_path=path, resume=True)
+    assert again["complete"] and all(again[k] == ref[k] for k in keys) and (again["perm"] == ref["perm"]).all()
+    o = orc.bnb(inst.F, inst.D, T=2, sb_iters=sb)
+    assert ref["opt"] == o["opt"] and ref["bounded"] == o["bounded"]
+    other = qapgen.taib(9, 5)
+    h2 = pkg.qap_rlt2_create(9, other.F, other.D)
+    with pytest.raises(pkg.QapError):
+        pkg.qap_bnb_run(h2, 2, batch=4, sb_iters=sb, checkpoint_path=path, resume=True)
+    pkg.qap_destroy(h2)
+    pkg.qap_destroy(h)
