@@ -122,26 +122,11 @@ __device__ __forceinline__ int64_t bid_of(const Geom &g, int i, int j, int k, in
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 template <int CPL>
-__device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const int (&poff)[CPL], uint32_t freemask,
-                                            int &j1, bool &j1free, double &delta)
+__device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const int (&poff)[CPL], int &j1, bool &j1free,
+                                            double &delta)
 {
-    if (CPL == 1) {
-        // min over the order key's high word; the low word only decides among equal high
-        // words (warp-uniform branch); then prefer a free column, then the lowest index.
-        const uint64_t key = okey(minv[0]);
-        const uint32_t hi = static_cast<uint32_t>(key >> 32);
-        const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
-        uint32_t bal = __ballot_sync(FULL_MASK, hi == mhi);
-        if (__popc(bal) > 1) {
-            const uint32_t lo = static_cast<uint32_t>(key);
-            const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
-            bal = __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
-        }
-        const uint32_t ft = bal & freemask;
-        j1 = __ffs(ft ? ft : bal) - 1;
-        j1free = ft != 0;
-        delta = __shfl_sync(FULL_MASK, minv[0], j1);
-    } else {
+    static_assert(CPL > 1, "CPL == 1 uses warp_lap_solve1");
+    {
         // lane-local best by (key, matched, t), then warp-wide
         uint64_t key = ~0ull;
         int rank = 0xff;
@@ -200,7 +185,6 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
         int j0 = -1, i0off = i * rowb;
         double ui0 = 0.0;
         int jfree;
-        const uint32_t freemask = __ballot_sync(FULL_MASK, poff[0] < 0 && lane < m);  // CPL == 1 only
         while (true) {
             const double *row = reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off);
 #pragma unroll
@@ -214,7 +198,7 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
             int j1;
             bool j1free;
             double delta;
-            warp_argmin<CPL>(minv, poff, freemask, j1, j1free, delta);
+            warp_argmin<CPL>(minv, poff, j1, j1free, delta);
             // next row to scan (used only if j1 is matched): fetched with the same lane group
             // as delta; ucol[j1] is not touched by this step's update (j1 is not yet settled)
             const int src = j1 & 31, tt = j1 >> 5;
@@ -283,6 +267,75 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
     }
 }
 
+// One column per lane (m <= 32): the same algorithm and the same floating-point
+// operations as warp_lap_solve<CPL>, with the column id equal to the lane id.  The
+// argmin takes the order key's high word first (the low word only on ties, a warp-uniform
+// branch), then prefers a free column (a lane mask updated once per augmentation), then
+// the lowest lane; the augmenting path is collected as one lane mask.
+template <bool COUNT>
+__device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int lane, int &poff, double &v,
+                                                double &ucol, int &steps)
+{
+    v = 0.0;
+    ucol = 0.0;
+    poff = -1;
+    int way = -1;
+    const int rowb = m * 8;
+    const double minv0 = lane < m ? CUDART_INF : qnan();
+    uint32_t freemask = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
+        double ucur = 0.0, ui0 = 0.0, minv = minv0, du = 0.0;
+        int j0 = -1, i0off = i * rowb, j1;
+#pragma unroll 2
+        for (;;) {
+            const double cur = (*reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off) - ui0) - v;
+            if (cur < minv) {  // false for settled columns (minv = NaN)
+                minv = cur;
+                way = j0;
+            }
+            // argmin of (minv, matched?, column): high word of the order key first
+            const uint32_t hb = static_cast<uint32_t>(__double2hiint(minv));
+            const uint32_t sg = static_cast<uint32_t>(static_cast<int32_t>(hb) >> 31);
+            const uint32_t hi = hb ^ (sg | 0x80000000u);
+            const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
+            uint32_t bal = __ballot_sync(FULL_MASK, hi == mhi);
+            if (bal & (bal - 1u)) {
+                const uint32_t lo = static_cast<uint32_t>(__double2loint(minv)) ^ sg;
+                const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
+                bal = __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
+            }
+            const uint32_t ft = bal & freemask;
+            j1 = __ffs(ft ? ft : bal) - 1;
+            const double delta = __shfl_sync(FULL_MASK, minv, j1);
+            const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
+            const double nx_u = __shfl_sync(FULL_MASK, ucol, j1);
+            ucur += delta;
+            minv -= delta;                  // NaN stays NaN on settled columns
+            ucol = fma(delta, du, ucol);    // settled: u[p[j]] += delta (exact product)
+            v = fma(-delta, du, v);         // settled: v[j] -= delta
+            if (lane == j1) {               // settle column j1: only the high words change
+                du = __hiloint2double(0x3ff00000, __double2loint(du));
+                minv = __hiloint2double(0x7ff80000, __double2loint(minv));
+            }
+            if (COUNT) steps++;
+            if (ft) break;
+            i0off = nx_off;
+            ui0 = nx_u;
+            j0 = j1;
+        }
+        // augment along way[]: columns on the path take the row (and its u) of way[c]
+        freemask &= ~(1u << j1);
+        uint32_t onmask = 0u;
+        for (int c = j1; c >= 0; c = __shfl_sync(FULL_MASK, way, c)) onmask |= 1u << c;
+        const int sp = __shfl_sync(FULL_MASK, poff, way);
+        const double su = __shfl_sync(FULL_MASK, ucol, way);
+        if ((onmask >> lane) & 1u) {
+            poff = way >= 0 ? sp : i * rowb;
+            ucol = way >= 0 ? su : ucur;
+        }
+    }
+}
+
 // Residual (reading R8), written IN PLACE over the smem cost block, + primal value S
 // (reading R9).  Returns S (all lanes) and sets `bad` if some residual fell below -tau.
 // p[t] receives the matched row of each owned column.  One pass: the clamp to +0 is
@@ -305,7 +358,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
         }
     }
     __syncwarp();
-    double mn = 0.0;
+    bool neg = false;  // some raw residual below -1e-9 (<= -tau candidates)
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         const int c = lane + 32 * t;
@@ -315,7 +368,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
 #pragma unroll 4
             for (int r = 0; r < m; r++) {
                 const double x = (Mc[r * m] - urow[r]) - vc;
-                mn = x < mn ? x : mn;
+                neg |= x < -1e-9;
                 Mc[r * m] = x > 0.0 ? x : 0.0;  // x <= 0 (incl. -0) -> +0
             }
             Mc[p[t] * m] = 0.0;  // assigned cell -> +0
@@ -326,13 +379,19 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
         for (int r = 0; r < m; r++) S = S + sel[r];  // sequential row order (reading R9)
     S = __shfl_sync(FULL_MASK, S, 0);
     bad = false;
-    if (__any_sync(FULL_MASK, mn < -1e-9)) {  // rare: exact test tau = 1e-9 max(1, max|M|)
-        double mx = 0.0;
+    if (__any_sync(FULL_MASK, neg)) {  // rare: exact test tau = 1e-9 max(1, max|M|)
+        // recompute the raw residuals from the original block (same operations)
+        double mx = 0.0, mn = 0.0;
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             const int c = lane + 32 * t;
             if (c < m)
-                for (int r = 0; r < m; r++) mx = fmax(mx, fabs(Mg[r * m + c]));
+                for (int r = 0; r < m; r++) {
+                    const double g = Mg[r * m + c];
+                    const double x = (g - urow[r]) - v[t];
+                    mn = x < mn ? x : mn;
+                    mx = fmax(mx, fabs(g));
+                }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -469,8 +528,13 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         int poff[CPL], p[CPL];
         double v[CPL], ucol[CPL];
         int steps = 0;
-        if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M + lane, m, lane, poff, v, ucol, steps);
-        else warp_lap_solve<CPL, false>(M + lane, m, lane, poff, v, ucol, steps);
+        if constexpr (CPL == 1) {
+            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M + lane, m, lane, poff[0], v[0], ucol[0], steps);
+            else warp_lap_solve1<false>(M + lane, m, lane, poff[0], v[0], ucol[0], steps);
+        } else {
+            if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M + lane, m, lane, poff, v, ucol, steps);
+            else warp_lap_solve<CPL, false>(M + lane, m, lane, poff, v, ucol, steps);
+        }
         bool bad;
         const double S = warp_lap_epilogue<CPL>(M, a.src + b * a.ld, m, lane, poff, p, v, ucol, urow, sel, bad);
         anybad |= bad;
