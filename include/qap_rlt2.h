@@ -259,6 +259,36 @@ qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32
  *   makes exactly the decisions of an uninterrupted one.  out->complete = 1 when the tree
  *   is exhausted.
  */
+/*
+ * qap_bnb_node — an open B&B node: m fixed pairs (facility fac[t] at location loc[t],
+ *   0-based, N <= 64) and its RLT2 bound lb (NAN: not bounded yet).
+ */
+typedef struct {
+    int32_t m;
+    int32_t fac[64], loc[64];
+    double lb;
+} qap_bnb_node;
+
+/*
+ * Subtree-parallel B&B hooks ("at the first Branch, each cpu_thread takes a subtree
+ *   (or node) and execute a depth-first search.  When it finished your subtree, the
+ *   cpu_thread takes another node that has not been fathomed"; load balancing of
+ *   unbalanced subtrees).  The library runs one worker's search; the
+ *   scheduler handing nodes to workers belongs to the caller (one process per GPU with a
+ *   shared store, threads, ...).
+ *   qap_bnb_sync_fn: called every sync_every bounded nodes and whenever the worker's
+ *     incumbent improves, with local_best (-1: none) and its permutation (N entries, NULL
+ *     when none).  It writes *global_best (best objective known to any worker, -1: none),
+ *     which the worker then prunes with (LB > global_best - 1 + 1e-6), and returns how many
+ *     open nodes the scheduler wants donated (0: none; < 0: abort with QAP_E_STATE).
+ *   qap_bnb_donate_fn: receives each donated node (bounded, not pruned; the callee copies
+ *     it).  Donation gives away the unvisited children of the worker's shallowest expanded
+ *     nodes (the largest remaining subtrees), whole nodes at a time, until at least the
+ *     requested number went out; donated nodes count as bounded by the donor.
+ */
+typedef int32_t (*qap_bnb_sync_fn)(void *ctx, int64_t local_best, const int32_t *perm, int64_t *global_best);
+typedef void (*qap_bnb_donate_fn)(void *ctx, const qap_bnb_node *node);
+
 typedef struct {
     int32_t iters;            /* RLT2 iterations per node                               */
     double K, UB0;            /* stop parameter, initial upper bound (+INFINITY: none)  */
@@ -268,6 +298,12 @@ typedef struct {
     int64_t checkpoint_every; /* bounded nodes between checkpoints (0: only on stop)    */
     int64_t max_nodes;        /* stop after this many bounded nodes (0: no limit)       */
     int32_t resume;
+    const qap_bnb_node *root; /* NULL: the instance root; else search only this subtree  */
+                              /* (root->lb not NAN: its bound, reused, not recounted)    */
+    qap_bnb_sync_fn sync;     /* NULL: none                                             */
+    qap_bnb_donate_fn donate; /* NULL: donation requests are ignored                    */
+    void *ctx;                /* passed to sync / donate                                */
+    int64_t sync_every;       /* bounded nodes between sync calls (<= 0: 32)            */
 } qap_bnb_opts;
 typedef struct {
     int64_t opt;              /* best objective found (-1: none better than UB0)        */
@@ -276,6 +312,20 @@ typedef struct {
     int32_t complete;
 } qap_bnb_result;
 qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *opts, qap_bnb_result *out);
+
+/*
+ * qap_bnb_frontier — breadth-first expansion from opts->root (NULL: the instance root)
+ *   with the rules of qap_bnb_solve (bounds, pruning, strong branching, leaves), level by
+ *   level, until a level holds >= target open nodes or the tree is exhausted (the first
+ *   phase of the subtree-parallel search).  On a sharded handle (world > 1) every
+ *   rank makes the same call and gets the same nodes; opts->batch > 1 needs a single-GPU
+ *   handle.  Writes the open nodes of the last level, in DFS order, to nodes[0..*n_nodes)
+ *   (HOST, capacity cap; QAP_E_CAPACITY if more) and the incumbent and counters of the
+ *   expansion to *out (out->complete = 1 when no open node is left).  Checkpoint, sync
+ *   and donate fields of opts are ignored.
+ */
+qap_status qap_bnb_frontier(qap_rlt2 *h, const qap_bnb_opts *opts, int32_t target, qap_bnb_node *nodes,
+                            int32_t cap, int32_t *n_nodes, qap_bnb_result *out);
 
 /*
  * qap_rlt2_strong_branch — strong branching with the RLT1 dual: every candidate

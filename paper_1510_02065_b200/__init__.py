@@ -33,13 +33,22 @@ EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
            "qap_destroy", "qap_lap_batch", "qap_bnb_solve", "qap_nccl_unique_id", "qap_rlt2_shard_info",
            "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound", "qap_rlt2_bound_async",
-           "qap_rlt2_bound_result", "qap_rlt2_strong_branch", "qap_bnb_run"]
+           "qap_rlt2_bound_result", "qap_rlt2_strong_branch", "qap_bnb_run", "qap_bnb_frontier"]
+
+
+class _BnbNode(ct.Structure):
+    _fields_ = [("m", ct.c_int32), ("fac", ct.c_int32 * 64), ("loc", ct.c_int32 * 64), ("lb", ct.c_double)]
+
+
+_SyncFn = ct.CFUNCTYPE(ct.c_int32, ct.c_void_p, ct.c_int64, ct.POINTER(ct.c_int32), ct.POINTER(ct.c_int64))
+_DonateFn = ct.CFUNCTYPE(None, ct.c_void_p, ct.POINTER(_BnbNode))
 
 
 class _BnbOpts(ct.Structure):
     _fields_ = [("iters", ct.c_int32), ("K", ct.c_double), ("UB0", ct.c_double), ("batch", ct.c_int32),
                 ("sb_iters", ct.c_int32), ("checkpoint_path", ct.c_char_p), ("checkpoint_every", ct.c_int64),
-                ("max_nodes", ct.c_int64), ("resume", ct.c_int32)]
+                ("max_nodes", ct.c_int64), ("resume", ct.c_int32), ("root", ct.POINTER(_BnbNode)),
+                ("sync", _SyncFn), ("donate", _DonateFn), ("ctx", ct.c_void_p), ("sync_every", ct.c_int64)]
 
 
 class _BnbResult(ct.Structure):
@@ -95,6 +104,7 @@ def load_library(path: str = LIB_PATH):
                                 ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
     L.qap_rlt2_strong_branch.argtypes = [vp, i32, vp, ct.POINTER(i32), ct.POINTER(i32)]
     L.qap_bnb_run.argtypes = [vp, ct.POINTER(_BnbOpts), ct.POINTER(_BnbResult)]
+    L.qap_bnb_frontier.argtypes = [vp, ct.POINTER(_BnbOpts), i32, vp, i32, ct.POINTER(i32), ct.POINTER(_BnbResult)]
     L.qap_rlt2_bound_async.argtypes = [vp, i32, f64, f64]
     L.qap_rlt2_bound_result.argtypes = [vp, ct.POINTER(_Result)]
     L.qap_nccl_unique_id.argtypes = [vp]
@@ -128,9 +138,10 @@ def _current_stream():
 class Handle:
     """Owner of a qap_rlt2* handle."""
 
-    def __init__(self, ptr, N: int):
+    def __init__(self, ptr, N: int, world: int = 1):
         self.ptr = ptr
         self.N = N
+        self.world = world  # > 1: a shard of a bound shared by `world` processes
 
     def close(self):
         if self.ptr:
@@ -165,7 +176,7 @@ def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0,
     out = ct.c_void_p()
     st = L.qap_rlt2_create(N, F.ctypes.data, D.ctypes.data, ct.byref(opts), ct.byref(out))
     _check(st, None)
-    return Handle(out.value, N)
+    return Handle(out.value, N, world)
 
 
 def qap_rlt2_load(h: Handle, F, D) -> None:
@@ -267,16 +278,80 @@ def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, 
     return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
 
 
-def qap_bnb_run(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
-                sb_iters: int = -1, checkpoint_path: str | None = None, checkpoint_every: int = 0,
-                max_nodes: int = 0, resume: bool = False) -> dict:
-    """B&B with checkpoint/resume (see include/qap_rlt2.h)."""
-    o = _BnbOpts(iters, K, UB0, batch, sb_iters, checkpoint_path.encode() if checkpoint_path else None,
-                 checkpoint_every, max_nodes, int(resume))
-    r = _BnbResult()
-    _check(load_library().qap_bnb_run(h.ptr, ct.byref(o), ct.byref(r)), h)
+def _node_in(nd: dict | None):
+    """{"fac": [...], "loc": [...], "lb": float | nan} -> _BnbNode (or None)."""
+    if nd is None:
+        return None
+    x = _BnbNode()
+    x.m = len(nd["fac"])
+    if x.m != len(nd["loc"]) or x.m > 64:
+        raise ValueError("node: fac and loc of equal length <= 64")
+    for t in range(x.m):
+        x.fac[t], x.loc[t] = int(nd["fac"][t]), int(nd["loc"][t])
+    x.lb = float(nd.get("lb", math.nan))
+    return x
+
+
+def _node_out(x) -> dict:
+    return dict(fac=[x.fac[t] for t in range(x.m)], loc=[x.loc[t] for t in range(x.m)], lb=x.lb)
+
+
+def _result_out(h: Handle, r) -> dict:
     return dict(opt=r.opt, perm=np.array(r.perm[: h.N], np.int32), bounded=r.bounded, leaves=r.leaves,
                 pruned=r.pruned, sb_cut=r.sb_cut, complete=bool(r.complete))
+
+
+def qap_bnb_run(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
+                sb_iters: int = -1, checkpoint_path: str | None = None, checkpoint_every: int = 0,
+                max_nodes: int = 0, resume: bool = False, root: dict | None = None, sync=None, donate=None,
+                sync_every: int = 0) -> dict:
+    """B&B with checkpoint/resume and the subtree-parallel hooks (include/qap_rlt2.h).
+    root: {"fac", "loc", "lb"} — search only that subtree.  sync(local_best, perm | None) ->
+    (global_best, n_donate); donate(node dict).  Exceptions raised in a callback abort the run
+    and are re-raised here."""
+    err = []
+
+    def _sync(_ctx, best, perm, gout):
+        try:
+            g, k = sync(int(best), np.ctypeslib.as_array(perm, (h.N,)).copy() if perm else None)
+            gout[0] = int(g)
+            return int(k)
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            err.append(e)
+            return -1
+
+    def _donate(_ctx, nd):
+        try:
+            donate(_node_out(nd.contents))
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    rn = _node_in(root)
+    cs = _SyncFn(_sync) if sync else _SyncFn()
+    cd = _DonateFn(_donate) if donate else _DonateFn()
+    o = _BnbOpts(iters, K, UB0, batch, sb_iters, checkpoint_path.encode() if checkpoint_path else None,
+                 checkpoint_every, max_nodes, int(resume), ct.pointer(rn) if rn is not None else None, cs, cd, None,
+                 sync_every)
+    r = _BnbResult()
+    st = load_library().qap_bnb_run(h.ptr, ct.byref(o), ct.byref(r))
+    if err:
+        raise err[0]
+    _check(st, h)
+    return _result_out(h, r)
+
+
+def qap_bnb_frontier(h: Handle, iters: int, target: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
+                     sb_iters: int = -1, root: dict | None = None, cap: int = 1 << 16):
+    """Breadth-first expansion until a level holds >= target open nodes (include/qap_rlt2.h).
+    Returns (open nodes in DFS order, result dict of the expansion)."""
+    rn = _node_in(root)
+    o = _BnbOpts(iters, K, UB0, batch, sb_iters, None, 0, 0, 0, ct.pointer(rn) if rn is not None else None,
+                 _SyncFn(), _DonateFn(), None, 0)
+    nodes = (_BnbNode * cap)()
+    n = ct.c_int32()
+    r = _BnbResult()
+    _check(load_library().qap_bnb_frontier(h.ptr, ct.byref(o), target, nodes, cap, ct.byref(n), ct.byref(r)), h)
+    return [_node_out(nodes[k]) for k in range(n.value)], _result_out(h, r)
 
 
 def qap_rlt2_strong_branch(h: Handle, sb_iters: int = 1):

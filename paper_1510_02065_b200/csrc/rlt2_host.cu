@@ -884,7 +884,14 @@ struct Bnb {
     std::vector<Frame> stack;
     bool root_done = false;
     qap_status st = QAP_OK;
+    // subtree-parallel hooks (include/qap_rlt2.h, NEXT-2)
+    qap_bnb_sync_fn sync_fn = nullptr;
+    qap_bnb_donate_fn donate_fn = nullptr;
+    void *ctx = nullptr;
+    int64_t sync_every = 32, since_sync = 0;
+    bool improved = false;
     const qap_rlt2 *h0() const { return pool[0]; }
+    bool cut(double lb) const { return lb > UB - 1.0 + 1e-6; }  // prune rule (R15)
 
     int64_t cost(const std::vector<int32_t> &perm) const
     {
@@ -902,6 +909,7 @@ struct Bnb {
                 best = v;
                 have = true;
                 best_perm = perm;
+                improved = true;
                 if ((double)v < UB) UB = (double)v;
             }
             return;
@@ -1017,6 +1025,83 @@ struct Bnb {
         Frame F;
         if (!make_frame(fac, loc, F)) return;
         stack.push_back(std::move(F));
+    }
+    // search only the subtree of `root` (its bound reused when given)
+    void start_at(const qap_bnb_node *root)
+    {
+        if (!root) {
+            start();
+            return;
+        }
+        root_done = true;
+        std::vector<int32_t> fac(root->fac, root->fac + root->m), loc(root->loc, root->loc + root->m);
+        if (N - root->m <= 3) {
+            leaf(fac, loc);
+            return;
+        }
+        double lb = root->lb;
+        if (std::isnan(lb)) {
+            if ((st = qap_rlt2_fix(pool[0], root->m, fac.data(), loc.data())) != QAP_OK) return;
+            qap_rlt2_result r{};
+            if ((st = qap_rlt2_bound(pool[0], iters, K, UB, &r)) != QAP_OK) return;
+            bounded++;
+            lb = r.lb;
+        }
+        if (cut(lb)) {
+            pruned++;
+            return;
+        }
+        Frame F;
+        if (!make_frame(fac, loc, F)) return;
+        stack.push_back(std::move(F));
+    }
+    // give away the unvisited children of the shallowest expanded nodes (largest subtrees)
+    // until at least k went out; they count as bounded (and pruned / cut) here
+    void donate(int64_t k)
+    {
+        int64_t given = 0;
+        for (size_t d = 0; d < stack.size() && given < k; d++) {
+            Frame &F = stack[d];
+            if (F.child_leaf || F.next >= F.fs.size()) continue;  // leaves are cheap: keep them
+            for (uint32_t c = F.next; c < F.fs.size(); c++) {
+                if (cut(F.est[c])) {
+                    sb_cut++;
+                    continue;
+                }
+                bounded++;
+                if (cut(F.lb[c])) {
+                    pruned++;
+                    continue;
+                }
+                qap_bnb_node nd{};
+                nd.m = (int32_t)F.fac.size() + 1;
+                for (size_t t = 0; t < F.fac.size(); t++) {
+                    nd.fac[t] = F.fac[t];
+                    nd.loc[t] = F.loc[t];
+                }
+                nd.fac[nd.m - 1] = F.fs[c];
+                nd.loc[nd.m - 1] = F.ls[c];
+                nd.lb = F.lb[c];
+                donate_fn(ctx, &nd);
+                given++;
+            }
+            F.next = (uint32_t)F.fs.size();
+        }
+    }
+    // exchange the incumbent with the scheduler; false: abort requested
+    bool sync()
+    {
+        since_sync = 0;
+        improved = false;
+        int64_t g = -1;
+        const int32_t k = sync_fn(ctx, have ? best : -1, have ? best_perm.data() : nullptr, &g);
+        if (k < 0) {
+            st = QAP_E_STATE;
+            return false;
+        }
+        if (g >= 0 && (double)g < UB) UB = (double)g;
+        if (k > 0 && donate_fn) donate(k);
+        return true;
     }
     // advance by one child; false when the search is over
     bool step()
@@ -1211,17 +1296,25 @@ bool load_checkpoint(Bnb &B, const char *path, std::string &err)
     B.root_done = true;
     return true;
 }
-}  // namespace
 
-extern "C" {
-
-qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
+// validated node (N <= 64, distinct facilities and locations in range)
+bool node_ok(const qap_rlt2 *h, const qap_bnb_node *nd)
 {
-    if (!h || !o || !out || o->iters < 0) return QAP_E_ARG;
+    if (nd->m < 0 || nd->m > h->N || h->N > 64) return false;
+    std::vector<char> uf(h->N, 0), ul(h->N, 0);
+    for (int t = 0; t < nd->m; t++) {
+        const int f = nd->fac[t], l = nd->loc[t];
+        if (f < 0 || f >= h->N || l < 0 || l >= h->N || uf[f] || ul[l]) return false;
+        uf[f] = ul[l] = 1;
+    }
+    return true;
+}
+
+// the caller's handle plus batch-1 helper handles, each on its own stream
+qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
+{
     if (h->world > 1 && o->batch > 1) return fail(h, QAP_E_ARG, "batched B&B needs a single-GPU handle");
-    if ((o->resume || o->checkpoint_every > 0) && !o->checkpoint_path)
-        return fail(h, QAP_E_ARG, "checkpointing needs checkpoint_path");
-    Bnb b;
+    if (o->root && !node_ok(h, o->root)) return fail(h, QAP_E_ARG, "invalid root node");
     b.pool.push_back(h);
     b.N = h->N;
     b.iters = o->iters;
@@ -1229,7 +1322,7 @@ qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
     b.UB = b.UB0 = o->UB0;
     b.sb_iters = o->sb_iters;
     const int B = o->batch < 1 ? 1 : (o->batch > b.N ? b.N : o->batch);
-    for (int k = 1; k < B; k++) {  // helper handles, each on its own stream
+    for (int k = 1; k < B; k++) {
         cudaStream_t s = nullptr;
         cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_fail(h, e, "bnb stream");
@@ -1244,13 +1337,43 @@ qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
         if (st != QAP_OK) return fail(h, st, std::string("bnb helper handle: ") + qap_last_error(nullptr));
         b.pool.push_back(x);
     }
+    return QAP_OK;
+}
+
+void bnb_out(const Bnb &b, bool done, qap_bnb_result *out)
+{
+    out->complete = done ? 1 : 0;
+    out->opt = b.have ? b.best : -1;
+    for (int x = 0; x < 64; x++) out->perm[x] = (b.have && x < b.N) ? b.best_perm[x] : -1;
+    out->bounded = b.bounded;
+    out->leaves = b.leaves;
+    out->pruned = b.pruned;
+    out->sb_cut = b.sb_cut;
+}
+}  // namespace
+
+extern "C" {
+
+qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
+{
+    if (!h || !o || !out || o->iters < 0) return QAP_E_ARG;
+    if ((o->resume || o->checkpoint_every > 0) && !o->checkpoint_path)
+        return fail(h, QAP_E_ARG, "checkpointing needs checkpoint_path");
+    Bnb b;
+    qap_status st0 = bnb_init(h, o, b);
+    if (st0 != QAP_OK) return st0;
+    b.sync_fn = o->sync;
+    b.donate_fn = o->donate;
+    b.ctx = o->ctx;
+    b.sync_every = o->sync_every > 0 ? o->sync_every : 32;
     std::string err;
     if (o->resume) {
         if (!load_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
     } else {
-        b.start();
+        b.start_at(o->root);
         if (b.st != QAP_OK) return b.st;
     }
+    if (b.sync_fn && !b.sync()) return fail(h, b.st, "bnb aborted by the sync callback");
     int64_t since = 0;
     bool done = false;
     const int64_t b0 = b.bounded;
@@ -1265,16 +1388,85 @@ qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
             since = 0;
             if (!save_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
         }
+        if (b.sync_fn && ((b.since_sync += b.bounded - before) >= b.sync_every || b.improved) && !b.sync())
+            return fail(h, b.st, "bnb aborted by the sync callback");
     }
     if (b.st != QAP_OK) return b.st;
+    if (b.sync_fn && !b.sync()) return fail(h, b.st, "bnb aborted by the sync callback");
     if (!done && o->checkpoint_path && !save_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
-    out->complete = done ? 1 : 0;
-    out->opt = b.have ? b.best : -1;
-    for (int x = 0; x < b.N && x < 64; x++) out->perm[x] = b.have ? b.best_perm[x] : -1;
-    out->bounded = b.bounded;
-    out->leaves = b.leaves;
-    out->pruned = b.pruned;
-    out->sb_cut = b.sb_cut;
+    bnb_out(b, done, out);
+    return QAP_OK;
+}
+
+qap_status qap_bnb_frontier(qap_rlt2 *h, const qap_bnb_opts *o, int32_t target, qap_bnb_node *nodes, int32_t cap,
+                            int32_t *n_nodes, qap_bnb_result *out)
+{
+    if (!h || !o || !out || !n_nodes || o->iters < 0 || cap < 0 || (cap > 0 && !nodes)) return QAP_E_ARG;
+    Bnb b;
+    qap_status st0 = bnb_init(h, o, b);
+    if (st0 != QAP_OK) return st0;
+    qap_bnb_node root{};
+    root.lb = NAN;
+    if (o->root) root = *o->root;
+    std::vector<qap_bnb_node> level;
+    auto vecs = [](const qap_bnb_node &nd, std::vector<int32_t> &fac, std::vector<int32_t> &loc) {
+        fac.assign(nd.fac, nd.fac + nd.m);
+        loc.assign(nd.loc, nd.loc + nd.m);
+    };
+    std::vector<int32_t> fac, loc;
+    vecs(root, fac, loc);
+    if (b.N - root.m <= 3) {
+        b.leaf(fac, loc);
+    } else {
+        if (std::isnan(root.lb)) {
+            if ((b.st = qap_rlt2_fix(h, root.m, fac.data(), loc.data())) != QAP_OK) return b.st;
+            qap_rlt2_result r{};
+            if ((b.st = qap_rlt2_bound(h, b.iters, b.K, b.UB, &r)) != QAP_OK) return b.st;
+            b.bounded++;
+            root.lb = r.lb;
+        }
+        if (b.cut(root.lb)) b.pruned++;
+        else level.push_back(root);
+    }
+    while (!level.empty() && (int64_t)level.size() < (int64_t)target) {
+        std::vector<qap_bnb_node> next;
+        for (const qap_bnb_node &nd : level) {
+            if (b.cut(nd.lb)) {  // the incumbent improved since nd was bounded
+                b.pruned++;
+                continue;
+            }
+            vecs(nd, fac, loc);
+            Frame F;
+            if (!b.make_frame(fac, loc, F)) return b.st;
+            for (size_t c = 0; c < F.fs.size(); c++) {
+                if (b.cut(F.est[c])) {
+                    b.sb_cut++;
+                    continue;
+                }
+                qap_bnb_node ch = nd;
+                ch.m = nd.m + 1;
+                ch.fac[nd.m] = F.fs[c];
+                ch.loc[nd.m] = F.ls[c];
+                if (F.child_leaf) {
+                    vecs(ch, fac, loc);
+                    b.leaf(fac, loc);
+                    continue;
+                }
+                b.bounded++;
+                if (b.cut(F.lb[c])) {
+                    b.pruned++;
+                    continue;
+                }
+                ch.lb = F.lb[c];
+                next.push_back(ch);
+            }
+        }
+        level.swap(next);
+    }
+    *n_nodes = (int32_t)level.size();
+    if ((int64_t)level.size() > (int64_t)cap) return fail(h, QAP_E_CAPACITY, "frontier larger than cap");
+    for (size_t k = 0; k < level.size(); k++) nodes[k] = level[k];
+    bnb_out(b, level.empty(), out);
     return QAP_OK;
 }
 

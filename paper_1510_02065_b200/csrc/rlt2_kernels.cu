@@ -19,6 +19,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "rlt2_internal.h"
 
 namespace rlt2 {
@@ -1023,8 +1025,28 @@ template <int CPL, int NBUF>
 static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
 {
     const size_t smem = lap_warp_smem(a.m, CPL, NBUF) * wpc;
-    cudaError_t e = cudaFuncSetAttribute(k_lap<CPL, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    // The dynamic-smem limit is a process-wide attribute of the kernel: raise it once per
+    // device to the opt-in maximum (setting it per launch to the exact size would race
+    // between threads launching different sizes, e.g. concurrent B&B workers).
+    static std::mutex mu;
+    static uint64_t done_dev = 0;
+    {
+        int dev = 0;
+        cudaError_t e0 = cudaGetDevice(&dev);
+        if (e0 != cudaSuccess) return e0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 64 || !((done_dev >> dev) & 1)) {
+            int mx = 0;
+            if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+                return e0;
+            if ((e0 = cudaFuncSetAttribute(k_lap<CPL, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
+                cudaSuccess)
+                return e0;
+            if (dev < 64) done_dev |= 1ull << dev;
+        }
+    }
+    if (smem > 232448) return cudaErrorInvalidValue;
+    cudaError_t e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF>, 32 * wpc, smem);
     if (e != cudaSuccess) return e;
