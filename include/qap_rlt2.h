@@ -237,8 +237,10 @@ qap_status qap_lap_batch(int32_t m, int64_t count, int64_t ld, const double *M_d
  *   solved by enumeration; prune when LB > UB - 1 + 1e-6; the incumbent is replaced
  *   only on strict improvement.  UB0 = +INFINITY for none.
  *   batch > 1: the children of an expanded node are bounded `batch` at a time
- *   concurrently (helper handles on their own streams, each sized like h); with K = 0
- *   every decision equals the one-node-at-a-time search.
+ *   concurrently (batch-1 helper handles on their own streams, each sized like h, owned by
+ *   h: created on first use, kept with their CUDA graphs for later calls, reloaded by
+ *   qap_rlt2_load and freed by qap_destroy); with K = 0 every decision equals the
+ *   one-node-at-a-time search.
  *   sb_iters >= 0: strong branching at nodes with n' >= 5: the line chosen by
  *   qap_rlt2_strong_branch is branched on (children in ascending order of the line's other
  *   index) and candidates whose RLT1 estimate exceeds UB - 1 + 1e-6 are cut (*sb_cut).

@@ -76,6 +76,10 @@ struct qap_rlt2 {
     // CUDA graphs of the iteration loop, keyed by (n, iterations, D still zero)
     cudaStream_t sCap = nullptr;
     std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+    // B&B helper handles (children bounded concurrently), each on its own stream: created
+    // on first use, kept (with their graphs) for later B&B calls, freed by qap_destroy
+    std::vector<qap_rlt2 *> bnb_helpers;
+    std::vector<cudaStream_t> bnb_streams;
 };
 
 static std::string g_create_error;
@@ -351,6 +355,8 @@ qap_status qap_rlt2_load(qap_rlt2 *h, const int64_t *F, const int64_t *D)
     if ((e = cudaMemcpyAsync(h->dF, F, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess ||
         (e = cudaMemcpyAsync(h->dDist, D, (size_t)N * N * 8, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess)
         return cuda_fail(h, e, "upload");
+    for (auto x : h->bnb_helpers)
+        if ((st = qap_rlt2_load(x, F, D)) != QAP_OK) return fail(h, st, "bnb helper reload");
     return qap_rlt2_fix(h, 0, nullptr, nullptr);
 }
 
@@ -828,6 +834,8 @@ const char *qap_last_error(const qap_rlt2 *h) { return h ? h->err.c_str() : g_cr
 void qap_destroy(qap_rlt2 *h)
 {
     if (!h) return;
+    for (auto x : h->bnb_helpers) qap_destroy(x);
+    for (auto s : h->bnb_streams) cudaStreamDestroy(s);
     cudaStreamSynchronize(h->stream);
     free_all(h);
     delete h;
@@ -873,8 +881,7 @@ struct Frame {
 };
 
 struct Bnb {
-    std::vector<qap_rlt2 *> pool;  // pool[0] = the caller's handle
-    std::vector<cudaStream_t> own_streams;
+    std::vector<qap_rlt2 *> pool;  // pool[0] = the caller's handle, then its B&B helpers
     int N = 0, iters = 0, sb_iters = -1;
     double K = 0.0, UB = INFINITY, UB0 = INFINITY;
     bool have = false;
@@ -1133,8 +1140,7 @@ struct Bnb {
     }
     ~Bnb()
     {
-        for (size_t k = 1; k < pool.size(); k++) qap_destroy(pool[k]);
-        for (auto s : own_streams) cudaStreamDestroy(s);
+        for (size_t k = 1; k < pool.size(); k++) cudaStreamSynchronize(pool[k]->stream);  // helpers: owned by h
     }
 };
 
@@ -1322,11 +1328,10 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
     b.UB = b.UB0 = o->UB0;
     b.sb_iters = o->sb_iters;
     const int B = o->batch < 1 ? 1 : (o->batch > b.N ? b.N : o->batch);
-    for (int k = 1; k < B; k++) {
+    while ((int)h->bnb_helpers.size() < B - 1) {
         cudaStream_t s = nullptr;
         cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_fail(h, e, "bnb stream");
-        b.own_streams.push_back(s);
         qap_rlt2_opts op{};
         op.device = h->device;
         op.cuda_stream = s;
@@ -1334,9 +1339,14 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
         op.lap_warps = h->lap_warps;
         qap_rlt2 *x = nullptr;
         qap_status st = qap_rlt2_create(h->N, h->F.data(), h->Dist.data(), &op, &x);
-        if (st != QAP_OK) return fail(h, st, std::string("bnb helper handle: ") + qap_last_error(nullptr));
-        b.pool.push_back(x);
+        if (st != QAP_OK) {
+            cudaStreamDestroy(s);
+            return fail(h, st, std::string("bnb helper handle: ") + qap_last_error(nullptr));
+        }
+        h->bnb_streams.push_back(s);
+        h->bnb_helpers.push_back(x);
     }
+    for (int k = 1; k < B; k++) b.pool.push_back(h->bnb_helpers[k - 1]);
     return QAP_OK;
 }
 
