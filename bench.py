@@ -28,6 +28,7 @@ METRIC = "RLT2 dual-ascent iters/s and LAPs/s at N=30 (1/2/4/8 B200); B&B nodes/
 N_DEFAULT, T_ITERS, SEED = 30, 20, 1
 BNB_ITERS = 10
 BNB_BATCH = 12
+SUB_N = 14  # subtree-parallel B&B instance (nug14-shaped)
 
 
 def n_stored(n):
@@ -322,6 +323,40 @@ def main():
                                     "nodes_per_s": rsb["bounded"] / dt2}}
     pkg.qap_destroy(h)
 
+    # subtree-parallel B&B: one worker per GPU on a larger tree;
+    # at N=1 the same instance by the batched DFS of one GPU (the scaling reference)
+    sub = None
+    if not args.no_bnb:
+        si = qapgen.nug(SUB_N, SEED)
+        hs = pkg.qap_rlt2_create(SUB_N, si.F, si.D, device=local_rank, stream=stream.cuda_stream)
+        if world > 1:
+            from paper_1510_02065_b200 import subtree
+            store = dist.PrefixStore("bench_subtree/", dist.distributed_c10d._get_default_store())
+            subtree.subtree_bnb(pkg, hs, store, rank, world, BNB_ITERS, batch=SUB_N, prefix="warm/")
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rsub = subtree.subtree_bnb(pkg, hs, store, rank, world, BNB_ITERS, batch=SUB_N, prefix="run/")
+            torch.cuda.synchronize()
+            t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dts = float(t.item())
+            sub = {"mode": f"subtree-parallel, {world} workers (one per GPU), frontier >= {4 * world} nodes, "
+                           f"task queue + incumbent sharing + donation over the torch.distributed store",
+                   "tasks": rsub["tasks"], "donated": rsub["donated"], "frontier_nodes": rsub["frontier_nodes"]}
+        else:
+            pkg.qap_bnb_solve(hs, BNB_ITERS, batch=SUB_N)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rsub = pkg.qap_bnb_solve(hs, BNB_ITERS, batch=SUB_N)
+            torch.cuda.synchronize()
+            dts = time.perf_counter() - t0
+            sub = {"mode": f"1 GPU: batched DFS ({SUB_N} children concurrently) — the reference for N>1"}
+        pkg.qap_destroy(hs)
+        sub.update({"config": f"nug{SUB_N}-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node",
+                    "opt": rsub["opt"], "bounded_nodes": rsub["bounded"], "seconds": dts,
+                    "nodes_per_s": rsub["bounded"] / dts, "timer": "host wall clock (max over ranks), after a warm-up"})
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -365,7 +400,7 @@ def main():
                     "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 80,
                     "path": "per step: qap_rlt2_load(pinned host F, D) + qap_rlt2_bound(T=20) "
                             "(result read back to the host)"},
-            "bnb": bnb,
+            "bnb": bnb, "bnb_subtree": sub,
             "gpu_launches": launches,
             "clocks": clk.summary()}
     if world == 1 and not args.no_cpu_baseline:
