@@ -14,6 +14,9 @@ Parity status per function (DESIGN.md §4 lists the pins):
                         instances reach OPT exactly; terminal values at N>=10 are
                         "parity unpinned" beyond these validity properties
   bnb                   pinned: optimum == brute-force optimum (N<=9)
+  fold (warm child)     pinned: preservation of every completion's cost and nonnegativity
+                        (exhaustive, n<=6), LB(child) >= LB(parent), warm B&B optimum ==
+                        brute force (tests/test_oracle_warm.py)
 """
 from __future__ import annotations
 
@@ -77,7 +80,9 @@ def lib():
             getattr(L, f).argtypes = [ct.c_void_p]
             getattr(L, f).restype = ct.POINTER(ct.c_double)
         L.oracle_state_free_maps.argtypes = [ct.c_void_p, _i32p, _i32p]
-        L.oracle_bnb.argtypes = [ct.c_int, _i64p, _i64p, ct.c_int, ct.c_double, ct.c_double, ct.c_int,
+        L.oracle_state_fold.restype = ct.c_void_p
+        L.oracle_state_fold.argtypes = [ct.c_void_p, ct.c_int, ct.c_int, ct.POINTER(ct.c_int)]
+        L.oracle_bnb.argtypes = [ct.c_int, _i64p, _i64p, ct.c_int, ct.c_double, ct.c_double, ct.c_int, ct.c_int,
                                  ct.POINTER(ct.c_int64), _i32p, ct.POINTER(ct.c_int64),
                                  ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]
         L.oracle_rlt1_iteration.argtypes = [ct.c_void_p, ct.POINTER(ct.c_double)]
@@ -234,6 +239,16 @@ class State:
         nD = self.sizes()[2]
         return self._arr(self._L.oracle_state_D, nD).reshape(-1, n - 2, n - 2)
 
+    def fold(self, a: int, b: int) -> "State":
+        """Warm child fixing reduced facility a at reduced location b (NEXT-3, reading R31)."""
+        err = ct.c_int()
+        h = self._L.oracle_state_fold(self._h, a, b, ct.byref(err))
+        if not h:
+            raise OracleError(f"oracle_state_fold failed with status {err.value}")
+        c = State.__new__(State)
+        c._L, c._h, c.N, c.n = self._L, h, self.N, self._L.oracle_state_n(h)
+        return c
+
     def free_maps(self):
         I = np.empty(self.n, np.int32)
         J = np.empty(self.n, np.int32)
@@ -246,16 +261,17 @@ def bound(F, Dist, T: int, K: float = 0.0, UB: float = math.inf, fixed=(), trace
     return s.bound(T, K, UB, trace=trace)
 
 
-def bnb(F, Dist, T: int = 3, K: float = 0.0, UB0: float = math.inf, sb_iters: int = -1):
+def bnb(F, Dist, T: int = 3, K: float = 0.0, UB0: float = math.inf, sb_iters: int = -1, warm: bool = False):
     """Minimal deterministic DFS branch-and-bound (strong branching with RLT1 when
-    sb_iters >= 0); returns dict(opt, perm, bounded, leaves, pruned, sb_cut)."""
+    sb_iters >= 0; warm children folded from the parent's state when warm); returns
+    dict(opt, perm, bounded, leaves, pruned, sb_cut)."""
     F = np.ascontiguousarray(F, dtype=np.int64)
     Dist = np.ascontiguousarray(Dist, dtype=np.int64)
     N = F.shape[0]
     best = ct.c_int64()
     perm = np.zeros(N, np.int32)
     b, l, p, c = ct.c_int64(), ct.c_int64(), ct.c_int64(), ct.c_int64()
-    _check(lib().oracle_bnb(N, F, Dist, T, K, UB0, sb_iters, ct.byref(best), perm, ct.byref(b), ct.byref(l),
+    _check(lib().oracle_bnb(N, F, Dist, T, K, UB0, sb_iters, int(warm), ct.byref(best), perm, ct.byref(b), ct.byref(l),
                             ct.byref(p), ct.byref(c)), "bnb")
     return dict(opt=best.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
 

@@ -287,6 +287,94 @@ ostate *oracle_state_new(int N, const int64_t *F, const int64_t *Dist, int nfix,
     return s;
 }
 
+/*
+ * Warm child (fold rules of SPEC S:368, derived in DESIGN.md
+ * reading R31 from the evaluation identity of P:169).  The child of node s fixing the
+ * reduced facility a at the reduced location b inherits s's dual state; every completion
+ * keeps its cost:
+ *   kappa' = kappa,  lb_dual' = lb_dual + b_ab
+ *   b'_xy      = (b_xy + c_ab[xy]) + c_xy[ab]
+ *   c'_xy[zw]  = c_xy[zw] + ((d_{ab,xy,zw} + d_{ab,zw,xy}) + d_{xy,zw,ab})    (logical d)
+ *   d'_{xy,zw}[pq] = d_{xy,zw}[pq]
+ * for x, z != a and y, w != b; child indices are the parent's with a and b removed.
+ * Entries of assignments that the fix makes infeasible (location b, facility a) are
+ * dropped.  The child is "fresh": its next bound starts with iteration 0 (concentrate
+ * C -> B -> LB), then the loop.  Returns NULL on bad arguments (*err).
+ */
+ostate *oracle_state_fold(const ostate *s, int a, int b, int *err)
+{
+    *err = ORC_E_ARG;
+    int n = s->n, n1 = n - 1;
+    if (n1 < 3 || a < 0 || a >= n || b < 0 || b >= n) return NULL;
+    ostate *c = calloc(1, sizeof(ostate));
+    c->N = s->N; c->n = n1; c->nfix = s->nfix + 1;
+    for (int t = 0; t < s->nfix; t++) { c->fac[t] = s->fac[t]; c->loc[t] = s->loc[t]; }
+    c->fac[s->nfix] = s->I[a]; c->loc[s->nfix] = s->J[b];
+    for (int x = 0; x < n1; x++) { c->I[x] = s->I[x + (x >= a)]; c->J[x] = s->J[x + (x >= b)]; }
+    c->kappa = s->kappa;
+    c->Fr = malloc(sizeof(int64_t) * n1 * n1);
+    c->Dr = malloc(sizeof(int64_t) * n1 * n1);
+    c->B0 = calloc((size_t)n1 * n1, sizeof(int64_t));
+    for (int x = 0; x < n1; x++)
+        for (int y = 0; y < n1; y++) {
+            c->Fr[x * n1 + y] = s->Fr[(x + (x >= a)) * n + (y + (y >= a))];
+            c->Dr[x * n1 + y] = s->Dr[(x + (x >= b)) * n + (y + (y >= b))];
+        }
+    c->nC = (int64_t)n1 * n1 * (n1 - 1) * (n1 - 1);
+    c->nblk = (int64_t)n1 * n1 * (n1 - 1) * (n1 - 1) / 2;
+    c->nD = c->nblk * (n1 - 2) * (n1 - 2);
+    c->blk = malloc(sizeof(int32_t) * (size_t)n1 * n1 * n1 * n1);
+    for (size_t t = 0; t < (size_t)n1 * n1 * n1 * n1; t++) c->blk[t] = -1;
+    int32_t id = 0;
+    for (int i = 0; i < n1; i++)
+        for (int j = 0; j < n1; j++)
+            for (int k = i + 1; k < n1; k++)
+                for (int l = 0; l < n1; l++)
+                    if (l != j) c->blk[((size_t)(i * n1 + j) * n1 + k) * n1 + l] = id++;
+    c->B = malloc(sizeof(double) * n1 * n1);
+    c->C = malloc(sizeof(double) * (size_t)c->nC);
+    c->D = malloc(sizeof(double) * (size_t)(c->nD > 0 ? c->nD : 1));
+    if (!c->B || !c->C || !c->D) { oracle_state_free(c); return NULL; }
+#define PX(x) ((x) + ((x) >= a))  /* child facility index -> parent */
+#define PY(y) ((y) + ((y) >= b))  /* child location index -> parent */
+    for (int x = 0; x < n1; x++)
+        for (int y = 0; y < n1; y++) {
+            int X = PX(x), Y = PY(y);
+            c->B[x * n1 + y] = (s->B[X * n + Y] + s->C[cidx(s, a, b, X, Y)]) + s->C[cidx(s, X, Y, a, b)];
+        }
+    for (int x = 0; x < n1; x++)
+        for (int y = 0; y < n1; y++)
+            for (int z = 0; z < n1; z++)
+                for (int w = 0; w < n1; w++) {
+                    if (z == x || w == y) continue;
+                    int X = PX(x), Y = PY(y), Z = PX(z), W = PY(w);
+                    double e1 = *dref(s, a, b, X, Y, Z, W);
+                    double e2 = *dref(s, a, b, Z, W, X, Y);
+                    double e3 = *dref(s, X, Y, Z, W, a, b);
+                    c->C[cidx(c, x, y, z, w)] = s->C[cidx(s, X, Y, Z, W)] + ((e1 + e2) + e3);
+                }
+    for (int x = 0; x < n1; x++)
+        for (int y = 0; y < n1; y++)
+            for (int z = x + 1; z < n1; z++)
+                for (int w = 0; w < n1; w++) {
+                    if (w == y) continue;
+                    for (int p = 0; p < n1; p++) {
+                        if (p == x || p == z) continue;
+                        for (int q = 0; q < n1; q++) {
+                            if (q == y || q == w) continue;
+                            *dref(c, x, y, z, w, p, q) = *dref(s, PX(x), PY(y), PX(z), PY(w), PX(p), PY(q));
+                        }
+                    }
+                }
+#undef PX
+#undef PY
+    c->lb_dual = s->lb_dual + s->B[a * n + b];
+    c->lb_glb = 0.0;
+    c->fresh = 1;
+    *err = ORC_OK;
+    return c;
+}
+
 /* ---- the operations of Algorithm 1 ---------------------------------------- */
 
 /* Cost concentration C -> B ("b_ij <- Concentrate(c_ij)"): for (i,j) in
@@ -580,6 +668,7 @@ typedef struct {
     int N;
     const int64_t *F, *Dist;
     int T;
+    int warm;            /* 1: children folded from the parent's post-bound state (NEXT-3)   */
     int sb_iters;        /* >= 0: strong branching with RLT1 (sb_iters iterations); < 0: off */
     int64_t sb_cut;      /* candidates cut by their RLT1 estimate                          */
     double K;
@@ -619,7 +708,8 @@ static void leaf_rec(bnb_ctx *c, int32_t *perm, const int32_t *ffac, int nf, int
     }
 }
 
-static void bnb_visit(bnb_ctx *c, int nfix, int32_t *fac, int32_t *loc)
+/* parent: the expanded parent's state (warm mode), the child fixing its reduced (pa, pb) */
+static void bnb_visit(bnb_ctx *c, int nfix, int32_t *fac, int32_t *loc, const ostate *parent, int pa, int pb)
 {
     if (c->err) return;
     int N = c->N;
@@ -637,47 +727,51 @@ static void bnb_visit(bnb_ctx *c, int nfix, int32_t *fac, int32_t *loc)
         return;
     }
     int err;
-    ostate *s = oracle_state_new(N, c->F, c->Dist, nfix, fac, loc, &err);
+    ostate *s = (c->warm && parent) ? oracle_state_fold(parent, pa, pb, &err)
+                                    : oracle_state_new(N, c->F, c->Dist, nfix, fac, loc, &err);
     if (!s) { c->err = err; return; }
     double LB; int iters, status;
     int st = oracle_bound(s, c->T, c->K, c->UB, &LB, NULL, &iters, &status, NULL);
-    oracle_state_free(s);
-    if (st) { c->err = st; return; }
+    if (st) { oracle_state_free(s); c->err = st; return; }
     c->bounded++;
-    if (LB > c->UB - 1.0 + 1e-6) { c->pruned++; return; }
+    if (LB > c->UB - 1.0 + 1e-6) { c->pruned++; oracle_state_free(s); return; }
+    if (!c->warm) { oracle_state_free(s); s = NULL; }  /* cold children: built from (F, D, fixed) */
+    const ostate *ps = s;  /* the children's parent state (warm mode) */
     if (c->sb_iters >= 0 && nf >= 5) {
         /* strong branching: branch on the row or column with the highest min-estimate;
            candidates whose RLT1 estimate already exceeds the incumbent are cut */
         double *est = malloc(sizeof(double) * nf * nf);
         int kind, index;
         int st2 = oracle_strong_branch(N, c->F, c->Dist, nfix, fac, loc, c->sb_iters, est, &kind, &index);
-        if (st2) { free(est); c->err = st2; return; }
+        if (st2) { free(est); oracle_state_free(s); c->err = st2; return; }
         for (int x = 0; x < nf; x++) {
             const int a = kind == 0 ? index : x, b = kind == 0 ? x : index;
             if (est[a * nf + b] > c->UB - 1.0 + 1e-6) { c->sb_cut++; continue; }
             fac[nfix] = ffac[a]; loc[nfix] = floc[b];
-            bnb_visit(c, nfix + 1, fac, loc);
+            bnb_visit(c, nfix + 1, fac, loc, ps, a, b);
         }
         free(est);
+        oracle_state_free(s);
         return;
     }
     int f = ffac[0];
     for (int x = 0; x < nl; x++) {
         fac[nfix] = f; loc[nfix] = floc[x];
-        bnb_visit(c, nfix + 1, fac, loc);
+        bnb_visit(c, nfix + 1, fac, loc, ps, 0, x);  /* f = ffac[0] is reduced facility 0 */
     }
+    oracle_state_free(s);
 }
 
 int oracle_bnb(int N, const int64_t *F, const int64_t *Dist, int T, double K, double UB0, int sb_iters,
-               int64_t *best_out, int32_t *perm_out, int64_t *bounded_out, int64_t *leaves_out,
+               int warm, int64_t *best_out, int32_t *perm_out, int64_t *bounded_out, int64_t *leaves_out,
                int64_t *pruned_out, int64_t *sb_cut_out)
 {
     if (N < 1 || N > 64) return ORC_E_ARG;
     bnb_ctx c;
     memset(&c, 0, sizeof c);
-    c.N = N; c.F = F; c.Dist = Dist; c.T = T; c.K = K; c.UB = UB0; c.sb_iters = sb_iters;
+    c.N = N; c.F = F; c.Dist = Dist; c.T = T; c.K = K; c.UB = UB0; c.sb_iters = sb_iters; c.warm = warm;
     int32_t fac[64], loc[64];
-    bnb_visit(&c, 0, fac, loc);
+    bnb_visit(&c, 0, fac, loc, NULL, 0, 0);
     if (c.err) return c.err;
     *best_out = c.have_best ? c.best : -1;
     if (c.have_best) memcpy(perm_out, c.best_perm, sizeof(int32_t) * N);
