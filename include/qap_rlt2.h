@@ -111,6 +111,24 @@ qap_status qap_rlt2_load(qap_rlt2 *h, const int64_t *F, const int64_t *D);
 qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_t *loc);
 
 /*
+ * qap_rlt2_fold — warm child (reading R31, fold rules of
+ *   SPEC S:368 derived from the evaluation identity P:169).  Makes `child`'s node the child
+ *   of `parent`'s node that fixes facility `fac` at location `loc` (original 0-based indices,
+ *   both free in the parent) and builds its dual state from the parent's CURRENT state
+ *   (after qap_rlt2_fix or a completed qap_rlt2_bound):
+ *     kappa' = kappa, lb_dual' = lb_dual + b_ab,
+ *     b'_xy = (b_xy + c_ab[xy]) + c_xy[ab],
+ *     c'_xy[zw] = c_xy[zw] + ((d_{ab,xy,zw} + d_{ab,zw,xy}) + d_{xy,zw,ab}),
+ *     D' = D restricted to the remaining indices,
+ *   so every completion keeps its cost.  The next qap_rlt2_bound(child, ...) runs iteration 0
+ *   (concentrate C -> B -> LB) and then the loop from that state.  Both handles: same device,
+ *   same instance, single-GPU; the parent needs n >= 4 free facilities.  Enqueued on the
+ *   child's stream, ordered after the parent's pending work and before its later work (no
+ *   host synchronisation).  Errors: QAP_E_ARG, QAP_E_STATE (parent mid-iteration).
+ */
+qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, int32_t loc);
+
+/*
  * qap_rlt2_bound — run Algorithm 1.
  *   If the node is fresh (after create/fix), iteration 0 (concentrate C->B->LB, reading
  *   R1) runs first; then up to max_iters iterations of the loop body P:185-193.  A later

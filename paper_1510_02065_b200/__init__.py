@@ -33,7 +33,7 @@ EXPORTS = ["qap_rlt2_create", "qap_rlt2_load", "qap_rlt2_fix", "qap_rlt2_bound",
            "qap_rlt2_dual_copy", "qap_rlt2_step", "qap_rlt2_kernel_stats", "qap_last_error",
            "qap_destroy", "qap_lap_batch", "qap_bnb_solve", "qap_nccl_unique_id", "qap_rlt2_shard_info",
            "qap_shard_plan", "qap_rlt2_create_group", "qap_rlt2_group_bound", "qap_rlt2_bound_async",
-           "qap_rlt2_bound_result", "qap_rlt2_strong_branch", "qap_bnb_run", "qap_bnb_frontier"]
+           "qap_rlt2_bound_result", "qap_rlt2_strong_branch", "qap_bnb_run", "qap_bnb_frontier", "qap_rlt2_fold"]
 
 
 class _BnbNode(ct.Structure):
@@ -104,6 +104,7 @@ def load_library(path: str = LIB_PATH):
                                 ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64)]
     L.qap_rlt2_strong_branch.argtypes = [vp, i32, vp, ct.POINTER(i32), ct.POINTER(i32)]
     L.qap_bnb_run.argtypes = [vp, ct.POINTER(_BnbOpts), ct.POINTER(_BnbResult)]
+    L.qap_rlt2_fold.argtypes = [vp, vp, i32, i32]
     L.qap_bnb_frontier.argtypes = [vp, ct.POINTER(_BnbOpts), i32, vp, i32, ct.POINTER(i32), ct.POINTER(_BnbResult)]
     L.qap_rlt2_bound_async.argtypes = [vp, i32, f64, f64]
     L.qap_rlt2_bound_result.argtypes = [vp, ct.POINTER(_Result)]
@@ -276,6 +277,12 @@ def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, 
     _check(load_library().qap_bnb_solve(h.ptr, iters, K, UB0, batch, sb_iters, ct.byref(opt), perm.ctypes.data,
                                         ct.byref(b), ct.byref(l), ct.byref(p), ct.byref(c)), h)
     return dict(opt=opt.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
+
+
+def qap_rlt2_fold(child: Handle, parent: Handle, fac: int, loc: int) -> None:
+    """Warm child: child's node := parent's node + (fac at loc), state folded from the
+    parent's current dual state (include/qap_rlt2.h, R31)."""
+    _check(load_library().qap_rlt2_fold(child.ptr, parent.ptr, fac, loc), child)
 
 
 def _node_in(nd: dict | None):

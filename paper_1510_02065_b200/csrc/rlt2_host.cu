@@ -418,6 +418,70 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
     return QAP_OK;
 }
 
+qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, int32_t loc)
+{
+    if (!child || !parent || child == parent) return child ? fail(child, QAP_E_ARG, "bad handles") : QAP_E_ARG;
+    if (child->world > 1 || parent->world > 1 || child->loopback || parent->loopback)
+        return fail(child, QAP_E_ARG, "fold needs single-GPU handles");
+    if (child->device != parent->device) return fail(child, QAP_E_ARG, "fold across devices");
+    if (child->N != parent->N || child->F != parent->F || child->Dist != parent->Dist)
+        return fail(child, QAP_E_ARG, "fold needs handles of the same instance");
+    if (parent->next_phase != PH_FRESH && parent->next_phase != QAP_PHASE_TRANSFER)
+        return fail(child, QAP_E_STATE, "parent is in the middle of an iteration");
+    const Node &pn = parent->node;
+    const int n = pn.n;
+    if (n - 1 < 3) return fail(child, QAP_E_ARG, "child would have fewer than 3 free facilities");
+    int a = -1, b = -1;
+    for (int x = 0; x < n; x++) {
+        if (pn.I[x] == fac) a = x;
+        if (pn.J[x] == loc) b = x;
+    }
+    if (a < 0 || b < 0) return fail(child, QAP_E_ARG, "facility or location not free in the parent");
+    Node nd = pn;
+    nd.m = pn.m + 1;
+    nd.n = n - 1;
+    nd.fac[pn.m] = fac;
+    nd.loc[pn.m] = loc;
+    for (int x = 0; x < n - 1; x++) {
+        nd.I[x] = pn.I[x + (x >= a)];
+        nd.J[x] = pn.J[x + (x >= b)];
+    }
+    cudaError_t e = cudaSetDevice(child->device);
+    if (e != cudaSuccess) return cuda_fail(child, e, "device");
+    // order: parent's pending work -> fold (child stream) -> later parent work
+    if ((e = cudaEventRecord(parent->evJoin, parent->stream)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(child->stream, parent->evJoin, 0)) != cudaSuccess)
+        return cuda_fail(child, e, "fold ordering");
+    child->node = nd;
+    make_geom(nd.n, child->geom);
+    child->call_launches = 0;
+    FoldArgs f{};
+    f.gp = parent->geom;
+    f.gc = child->geom;
+    f.a = a;
+    f.b = b;
+    f.pB = parent->dB;
+    f.pC = parent->dC;
+    f.pD = parent->dD;
+    f.pctl = parent->dCtl;
+    f.cB = child->dB;
+    f.cC = child->dC;
+    f.cD = child->dD;
+    f.cctl = child->dCtl;
+    f.triples = child->dTriples;
+    f.d_zero = parent->d_zero;
+    e = launch(child, QAP_K_INIT, child->stream, [&](cudaStream_t st) { return launch_fold(f, child->num_sms, st); });
+    if (e != cudaSuccess) return cuda_fail(child, e, "k_fold");
+    if ((e = cudaEventRecord(child->evJoin, child->stream)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(parent->stream, child->evJoin, 0)) != cudaSuccess)
+        return cuda_fail(child, e, "fold ordering");
+    child->next_phase = PH_FRESH;
+    child->d_zero = parent->d_zero;
+    child->b_zero = 0;
+    child->c_zero = 0;
+    return QAP_OK;
+}
+
 // Enqueue one phase of Algorithm 1.  `st` is the stream the call's work is ordered on.
 // In overlapped mode the TRANSFER phase runs on the low-priority stream sT and the level-2
 // LAP kernel (CONC_D) on the high-priority stream sL concurrently with it: LAP warps take

@@ -90,6 +90,19 @@ cudaError_t launch_rlt1_init(const Node &parent, const Rlt1Batch &R, const int64
 cudaError_t launch_rlt1_pair(const Rlt1Batch &R, cudaStream_t st);
 // level 1 (acc: iteration 0) or level 0 LAPs of every child
 cudaError_t launch_rlt1_lap(const Rlt1Batch &R, int level1, int acc, int num_sms, cudaStream_t st);
+// warm child (NEXT-3 (i)): parent state (gp) -> child state (gc, n = gp.n - 1)
+struct FoldArgs {
+    Geom gp, gc;
+    int a, b;  // parent-reduced facility / location fixed by the child
+    const double *pB, *pC, *pD;
+    const Ctl *pctl;
+    double *cB, *cC, *cD;
+    Ctl *cctl;
+    int *triples;  // child's facility-triples table
+    int d_zero;    // parent D lazily zero
+};
+cudaError_t launch_fold(const FoldArgs &f, int num_sms, cudaStream_t st);
+
 cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const int64_t *Dist,
                         double *B, double *C, int *triples, Ctl *ctl, cudaStream_t st);
 cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaStream_t st);

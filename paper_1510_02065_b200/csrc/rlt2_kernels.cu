@@ -640,26 +640,29 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
 // k_init — O0/O1: b0 with the fixed-free folds, c_ij[kl] = f'_ik d'_jl,
 // kappa; D is NOT written (the next transfer reads it as zero).
 // ---------------------------------------------------------------------------------------
+// facility triples i<k<p in lexicographic order (the transfer kernel's grid.y)
+__device__ void write_triples(int n, int *triples)
+{
+    const int ntri = n * (n - 1) * (n - 2) / 6;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += gridDim.x * blockDim.x) {
+        int rem = t, i = 0;
+        while (rem >= (n - 1 - i) * (n - 2 - i) / 2) {
+            rem -= (n - 1 - i) * (n - 2 - i) / 2;
+            i++;
+        }
+        int k = i + 1;
+        while (rem >= n - 1 - k) {
+            rem -= n - 1 - k;
+            k++;
+        }
+        triples[t] = i | (k << 8) | ((k + 1 + rem) << 16);
+    }
+}
+
 __global__ void k_init(const Node nd, const Geom g, const int64_t *__restrict__ F,
                        const int64_t *__restrict__ Dist, double *B, double *C, int *triples, Ctl *ctl)
 {
-    {  // facility triples i<k<p in lexicographic order (the transfer kernel's grid.y)
-        const int n = nd.n;
-        const int ntri = n * (n - 1) * (n - 2) / 6;
-        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += gridDim.x * blockDim.x) {
-            int rem = t, i = 0;
-            while (rem >= (n - 1 - i) * (n - 2 - i) / 2) {
-                rem -= (n - 1 - i) * (n - 2 - i) / 2;
-                i++;
-            }
-            int k = i + 1;
-            while (rem >= n - 1 - k) {
-                rem -= n - 1 - k;
-                k++;
-            }
-            triples[t] = i | (k << 8) | ((k + 1 + rem) << 16);
-        }
-    }
+    write_triples(nd.n, triples);
     const int N = nd.N, n = nd.n, n1 = n - 1;
     const int64_t n4 = (int64_t)n * n * n * n;
     const int64_t tot = n4 + (int64_t)n * n;
@@ -691,6 +694,105 @@ __global__ void k_init(const Node nd, const Geom g, const int64_t *__restrict__ 
         ctl->status = 0;
         ctl->stopped = 0;
         ctl->err = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Warm child (reading R31): the state of the child of the parent
+// node (gp: n free) that fixes the parent-reduced facility a at location b, built from the
+// parent's dual state:
+//   kappa' = kappa, lb_dual' = lb_dual + b_ab
+//   b'_xy     = (b_xy + c_ab[xy]) + c_xy[ab]
+//   c'_xy[zw] = c_xy[zw] + ((d_{ab,xy,zw} + d_{ab,zw,xy}) + d_{xy,zw,ab})   (logical d)
+//   d'_{xy,zw}[pq] = d_{xy,zw}[pq]                     (x,z != a; y,w != b; indices shifted)
+// k_fold_bc writes B', C', the child's control block and its triples table (one thread per
+// entry); k_fold_d copies the restricted D blocks (one warp per child block, lane = column,
+// rows streamed).  With the parent's D still lazily zero, the D terms are 0 and D' is left
+// lazily zero too.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t cidx_g(const Geom &g, int i, int j, int k, int l)
+{
+    return (int64_t)(i * g.n + j) * g.ldc + (int64_t)(k - (k > i)) * (g.n - 1) + (l - (l > j));
+}
+__device__ __forceinline__ double dlogical(const Geom &g, const double *D, int i, int j, int k, int l, int p, int q)
+{
+    if (i > k) {
+        int t = i;
+        i = k;
+        k = t;
+        t = j;
+        j = l;
+        l = t;
+    }
+    return D[bid_of(g, i, j, k, l) * g.ld2 + (int64_t)(p - (p > i) - (p > k)) * (g.n - 2) + (q - (q > j) - (q > l))];
+}
+
+__global__ void k_fold_bc(const FoldArgs f)
+{
+    const Geom &gp = f.gp;
+    const int n = gp.n, nc = n - 1, nc1 = nc - 1, a = f.a, b = f.b;
+    write_triples(nc, f.triples);
+    const int nC = nc * nc * nc1 * nc1, tot = nC + nc * nc;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+        if (t < nC) {
+            const int lw = t % nc1, kz = (t / nc1) % nc1, y = (t / (nc1 * nc1)) % nc, x = t / (nc1 * nc1 * nc);
+            const int z = kz + (kz >= x), w = lw + (lw >= y);  // child indices of the entry
+            const int X = x + (x >= a), Y = y + (y >= b), Z = z + (z >= a), W = w + (w >= b);
+            double e = 0.0;
+            if (!f.d_zero) {
+                const double e1 = dlogical(gp, f.pD, a, b, X, Y, Z, W);
+                const double e2 = dlogical(gp, f.pD, a, b, Z, W, X, Y);
+                const double e3 = dlogical(gp, f.pD, X, Y, Z, W, a, b);
+                e = (e1 + e2) + e3;
+            } else {
+                e = (0.0 + 0.0) + 0.0;
+            }
+            f.cC[(int64_t)(x * nc + y) * f.gc.ldc + (int64_t)kz * nc1 + lw] = f.pC[cidx_g(gp, X, Y, Z, W)] + e;
+        } else {
+            const int u = t - nC, x = u / nc, y = u % nc;
+            const int X = x + (x >= a), Y = y + (y >= b);
+            f.cB[u] = (f.pB[X * n + Y] + f.pC[cidx_g(gp, a, b, X, Y)]) + f.pC[cidx_g(gp, X, Y, a, b)];
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Ctl *c = f.cctl;
+        c->kappa = f.pctl->kappa;
+        c->lb_dual = f.pctl->lb_dual + f.pB[a * n + b];
+        c->lbprime = 0.0;
+        c->lb = (double)c->kappa + c->lb_dual;
+        c->lb_glb = c->lb;
+        c->iters = 0;
+        c->status = 0;
+        c->stopped = 0;
+        c->err = 0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_fold_d(const FoldArgs f)
+{
+    const Geom &gp = f.gp, &gc = f.gc;
+    const int nc = gc.n, nc1 = nc - 1, mc = nc - 2, mp = gp.n - 2, a = f.a, b = f.b;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int hint = 0;
+    for (int64_t cb = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); cb < gc.nblk; cb += nw) {
+        while (hint + 1 < nc && cb >= gc.off[hint + 1]) hint++;
+        while (hint > 0 && cb < gc.off[hint]) hint--;
+        const int x = hint;
+        int rem = (int)(cb - gc.off[x]);
+        const int per_y = (nc1 - x) * nc1;
+        const int y = rem / per_y;
+        rem -= y * per_y;
+        const int zz = rem / nc1, wl = rem - zz * nc1;
+        const int z = x + 1 + zz, w = wl + (wl >= y);
+        const int X = x + (x >= a), Y = y + (y >= b), Z = z + (z >= a), W = w + (w >= b);
+        const int ra = a - (a > X) - (a > Z), cbk = b - (b > Y) - (b > W);  // parent row/col dropped
+        const double *src = f.pD + bid_of(gp, X, Y, Z, W) * gp.ld2;
+        double *dst = f.cD + cb * gc.ld2;
+        for (int r = 0; r < mc; r++) {
+            const double *sr = src + (int64_t)(r + (r >= ra)) * mp;
+            for (int c = lane; c < mc; c += 32) dst[r * mc + c] = sr[c + (c >= cbk)];
+        }
     }
 }
 
@@ -978,6 +1080,21 @@ cudaError_t launch_init(const Node &node, const Geom &g, const int64_t *F, const
     int blocks = (int)((tot + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_init<<<blocks, 256, 0, st>>>(node, g, F, Dist, B, C, triples, ctl);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fold(const FoldArgs &f, int num_sms, cudaStream_t st)
+{
+    const int nc = f.gc.n;
+    const int64_t tot = (int64_t)nc * nc * (nc - 1) * (nc - 1) + (int64_t)nc * nc;
+    int blocks = (int)((tot + 255) / 256);
+    if (blocks > num_sms * 16) blocks = num_sms * 16;
+    k_fold_bc<<<blocks, 256, 0, st>>>(f);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || f.d_zero) return e;
+    int64_t wb = (f.gc.nblk + 7) / 8;
+    const int grid = (int)(wb < (int64_t)num_sms * 8 ? wb : (int64_t)num_sms * 8);
+    k_fold_d<<<grid, 256, 0, st>>>(f);
     return cudaGetLastError();
 }
 
