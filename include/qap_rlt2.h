@@ -278,6 +278,13 @@ qap_status qap_bnb_solve(qap_rlt2 *h, int32_t iters, double K, double UB0, int32
  *   from checkpoint_path (same instance and parameters, checked by digest); a resumed run
  *   makes exactly the decisions of an uninterrupted one.  out->complete = 1 when the tree
  *   is exhausted.
+ *   warm = 1 (NEXT-3 (i), reading R31): every child's state is folded from its parent's
+ *   post-bound state (qap_rlt2_fold) instead of rebuilt cold; the root (or `root`) is
+ *   bounded cold.  The states of the expanded nodes on the current DFS path are kept in
+ *   depth handles owned by h (capacity N - d each, created on first use); a node expanded
+ *   after its children were bounded concurrently has its state rebuilt (fold + the same
+ *   bound), so with K = 0 the decisions equal the one-node-at-a-time warm search (the
+ *   oracle's).  qap_bnb_frontier always bounds cold.
  */
 /*
  * qap_bnb_node — an open B&B node: m fixed pairs (facility fac[t] at location loc[t],
@@ -324,6 +331,8 @@ typedef struct {
     qap_bnb_donate_fn donate; /* NULL: donation requests are ignored                    */
     void *ctx;                /* passed to sync / donate                                */
     int64_t sync_every;       /* bounded nodes between sync calls (<= 0: 32)            */
+    int32_t warm;             /* 1: warm children (qap_rlt2_fold of the parent's state, */
+                              /* NEXT-3); 0: cold children (qap_rlt2_fix)                */
 } qap_bnb_opts;
 typedef struct {
     int64_t opt;              /* best objective found (-1: none better than UB0)        */

@@ -48,7 +48,8 @@ class _BnbOpts(ct.Structure):
     _fields_ = [("iters", ct.c_int32), ("K", ct.c_double), ("UB0", ct.c_double), ("batch", ct.c_int32),
                 ("sb_iters", ct.c_int32), ("checkpoint_path", ct.c_char_p), ("checkpoint_every", ct.c_int64),
                 ("max_nodes", ct.c_int64), ("resume", ct.c_int32), ("root", ct.POINTER(_BnbNode)),
-                ("sync", _SyncFn), ("donate", _DonateFn), ("ctx", ct.c_void_p), ("sync_every", ct.c_int64)]
+                ("sync", _SyncFn), ("donate", _DonateFn), ("ctx", ct.c_void_p), ("sync_every", ct.c_int64),
+                ("warm", ct.c_int32)]
 
 
 class _BnbResult(ct.Structure):
@@ -270,7 +271,11 @@ def qap_rlt2_bound_result(h: Handle) -> dict:
 
 
 def qap_bnb_solve(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
-                  sb_iters: int = -1) -> dict:
+                  sb_iters: int = -1, warm: bool = False) -> dict:
+    if warm:  # warm children: through qap_bnb_run (the C signature of qap_bnb_solve is cold-only)
+        r = qap_bnb_run(h, iters, K=K, UB0=UB0, batch=batch, sb_iters=sb_iters, warm=True)
+        r.pop("complete")
+        return r
     opt = ct.c_int64()
     perm = np.zeros(h.N, np.int32)
     b, l, p, c = ct.c_int64(), ct.c_int64(), ct.c_int64(), ct.c_int64()
@@ -311,7 +316,7 @@ def _result_out(h: Handle, r) -> dict:
 def qap_bnb_run(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,
                 sb_iters: int = -1, checkpoint_path: str | None = None, checkpoint_every: int = 0,
                 max_nodes: int = 0, resume: bool = False, root: dict | None = None, sync=None, donate=None,
-                sync_every: int = 0) -> dict:
+                sync_every: int = 0, warm: bool = False) -> dict:
     """B&B with checkpoint/resume and the subtree-parallel hooks (include/qap_rlt2.h).
     root: {"fac", "loc", "lb"} — search only that subtree.  sync(local_best, perm | None) ->
     (global_best, n_donate); donate(node dict).  Exceptions raised in a callback abort the run
@@ -338,7 +343,7 @@ def qap_bnb_run(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, ba
     cd = _DonateFn(_donate) if donate else _DonateFn()
     o = _BnbOpts(iters, K, UB0, batch, sb_iters, checkpoint_path.encode() if checkpoint_path else None,
                  checkpoint_every, max_nodes, int(resume), ct.pointer(rn) if rn is not None else None, cs, cd, None,
-                 sync_every)
+                 sync_every, int(warm))
     r = _BnbResult()
     st = load_library().qap_bnb_run(h.ptr, ct.byref(o), ct.byref(r))
     if err:
@@ -353,7 +358,7 @@ def qap_bnb_frontier(h: Handle, iters: int, target: int, K: float = 0.0, UB0: fl
     Returns (open nodes in DFS order, result dict of the expansion)."""
     rn = _node_in(root)
     o = _BnbOpts(iters, K, UB0, batch, sb_iters, None, 0, 0, 0, ct.pointer(rn) if rn is not None else None,
-                 _SyncFn(), _DonateFn(), None, 0)
+                 _SyncFn(), _DonateFn(), None, 0, 0)
     nodes = (_BnbNode * cap)()
     n = ct.c_int32()
     r = _BnbResult()

@@ -80,6 +80,10 @@ struct qap_rlt2 {
     // on first use, kept (with their graphs) for later B&B calls, freed by qap_destroy
     std::vector<qap_rlt2 *> bnb_helpers;
     std::vector<cudaStream_t> bnb_streams;
+    // warm B&B (NEXT-3): bnb_depth[d-1] holds the state of the expanded node at depth d of
+    // the current DFS path (capacity N - d, on this handle's stream)
+    std::vector<qap_rlt2 *> bnb_depth;
+    int n_cap = 0;  // largest node (free facilities) the buffers hold
 };
 
 static std::string g_create_error;
@@ -198,7 +202,7 @@ static qap_status check_instance(qap_rlt2 *h, int N, const int64_t *F, const int
 extern "C" {
 
 static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
-                              qap_rlt2 **out, bool loopback);
+                              qap_rlt2 **out, bool loopback, int n_cap = 0);
 
 qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
                            qap_rlt2 **out)
@@ -206,8 +210,9 @@ qap_status qap_rlt2_create(int32_t N, const int64_t *F, const int64_t *D, const 
     return create_impl(N, F, D, opts, out, false);
 }
 
+// n_cap (internal, single-GPU): buffers sized for nodes with at most n_cap free facilities
 static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
-                              qap_rlt2 **out, bool loopback)
+                              qap_rlt2 **out, bool loopback, int n_cap)
 {
     if (!out) return fail(nullptr, QAP_E_ARG, "out is NULL");
     *out = nullptr;
@@ -243,9 +248,10 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
     h->F.assign(F, F + (size_t)N * N);
     h->Dist.assign(D, D + (size_t)N * N);
+    h->n_cap = (n_cap >= 3 && n_cap < N && world == 1) ? n_cap : N;
 
     Geom gN;
-    make_geom(N, gN);
+    make_geom(h->n_cap, gN);
     size_t bytesD = (size_t)gN.nblk * gN.ld2 * 8;
     if (world > 1) {  // this rank's block slice, tile list and exchange slots: max over n <= N
         ShardPlan P;
@@ -261,8 +267,8 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         }
         bytesD = (size_t)(h->dblk_cap > 0 ? h->dblk_cap : 1) * gN.ld2 * 8;
     }
-    const size_t bytesC = (size_t)N * N * gN.ldc * 8;
-    const size_t bytesB = (((size_t)N * N + 1) & ~size_t(1)) * 8;
+    const size_t bytesC = (size_t)gN.n * gN.n * gN.ldc * 8;
+    const size_t bytesB = (((size_t)gN.n * gN.n + 1) & ~size_t(1)) * 8;
     const size_t bytesS = (size_t)gN.nblk * 8;
     size_t freeb = 0, totb = 0;
     if ((e = cudaMemGetInfo(&freeb, &totb)) != cudaSuccess) {
@@ -292,7 +298,7 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
     ALLOC(h->dSigma, bytesS);
     ALLOC(h->dTrace, (size_t)h->trace_cap * 8);
     ALLOC(h->dCtl, sizeof(Ctl));
-    ALLOC(h->dTriples, (size_t)N * (N - 1) * (N - 2) / 6 * sizeof(int) + 16);
+    ALLOC(h->dTriples, (size_t)gN.n * (gN.n - 1) * (gN.n - 2) / 6 * sizeof(int) + 16);
     ALLOC(h->dSched, sizeof(Sched));
     if (world > 1) {
         ALLOC(h->dTiles, h->tiles_cap * sizeof(int) + 16);
@@ -332,7 +338,8 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         delete h;
         return cuda_fail(nullptr, e, "upload");
     }
-    qap_status s = qap_rlt2_fix(h, 0, nullptr, nullptr);
+    // the root node (a capacity-limited internal handle gets its nodes by qap_rlt2_fold)
+    qap_status s = h->n_cap == N ? qap_rlt2_fix(h, 0, nullptr, nullptr) : QAP_OK;
     if (s != QAP_OK) {
         g_create_error = h->err;
         free_all(h);
@@ -357,6 +364,12 @@ qap_status qap_rlt2_load(qap_rlt2 *h, const int64_t *F, const int64_t *D)
         return cuda_fail(h, e, "upload");
     for (auto x : h->bnb_helpers)
         if ((st = qap_rlt2_load(x, F, D)) != QAP_OK) return fail(h, st, "bnb helper reload");
+    for (auto x : h->bnb_depth)
+        if ((st = qap_rlt2_load(x, F, D)) != QAP_OK) return fail(h, st, "bnb depth handle reload");
+    if (h->n_cap < N) {  // internal capacity-limited handle: no root node; fold gives it nodes
+        h->next_phase = PH_FRESH;
+        return QAP_OK;
+    }
     return qap_rlt2_fix(h, 0, nullptr, nullptr);
 }
 
@@ -365,6 +378,7 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
     if (!h) return QAP_E_ARG;
     const int N = h->N;
     if (m < 0 || N - m < 3) return fail(h, QAP_E_ARG, "need 0 <= m <= N-3");
+    if (N - m > h->n_cap) return fail(h, QAP_E_CAPACITY, "node larger than the handle's capacity");
     if (m > 0 && (!fac || !loc)) return fail(h, QAP_E_ARG, "fac/loc NULL");
     bool uf[kMaxN] = {false}, ul[kMaxN] = {false};
     for (int t = 0; t < m; t++) {
@@ -437,6 +451,7 @@ qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, i
         if (pn.J[x] == loc) b = x;
     }
     if (a < 0 || b < 0) return fail(child, QAP_E_ARG, "facility or location not free in the parent");
+    if (n - 1 > child->n_cap) return fail(child, QAP_E_CAPACITY, "child larger than the handle's capacity");
     Node nd = pn;
     nd.m = pn.m + 1;
     nd.n = n - 1;
@@ -673,6 +688,7 @@ qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double
         return fail(h, QAP_E_STATE, "bound called in the middle of an iteration");
     if (max_iters > h->trace_cap) return fail(h, QAP_E_ARG, "max_iters above the trace capacity (4096)");
     if (h->loopback) return fail(h, QAP_E_STATE, "in-process group member: use qap_rlt2_group_bound");
+    if (h->geom.n < 3) return fail(h, QAP_E_STATE, "the handle holds no node");
     h->call_launches = 0;
     cudaError_t e = launch_ctl_begin(h->dCtl, K, UB, h->trace_cap, h->stream);
     h->call_launches++;
@@ -900,6 +916,7 @@ void qap_destroy(qap_rlt2 *h)
     if (!h) return;
     for (auto x : h->bnb_helpers) qap_destroy(x);
     for (auto s : h->bnb_streams) cudaStreamDestroy(s);
+    for (auto x : h->bnb_depth) qap_destroy(x);
     cudaStreamSynchronize(h->stream);
     free_all(h);
     delete h;
@@ -945,7 +962,12 @@ struct Frame {
 };
 
 struct Bnb {
-    std::vector<qap_rlt2 *> pool;  // pool[0] = the caller's handle, then its B&B helpers
+    std::vector<qap_rlt2 *> pool;  // handles that bound children: cold: the caller's + helpers; warm: helpers
+    // warm children (NEXT-3 (i), reading R31): depth[d] holds the dual state of the expanded
+    // node with base_m + d fixed pairs on the current DFS path (depth[0] = the caller's handle)
+    bool warm = false;
+    int base_m = 0;
+    std::vector<qap_rlt2 *> depth;
     int N = 0, iters = 0, sb_iters = -1;
     double K = 0.0, UB = INFINITY, UB0 = INFINITY;
     bool have = false;
@@ -961,7 +983,7 @@ struct Bnb {
     void *ctx = nullptr;
     int64_t sync_every = 32, since_sync = 0;
     bool improved = false;
-    const qap_rlt2 *h0() const { return pool[0]; }
+    const qap_rlt2 *h0() const { return depth[0]; }  // the caller's handle
     bool cut(double lb) const { return lb > UB - 1.0 + 1e-6; }  // prune rule (R15)
 
     int64_t cost(const std::vector<int32_t> &perm) const
@@ -1026,11 +1048,15 @@ struct Bnb {
             const size_t c1 = c0 + B < idx.size() ? c0 + B : idx.size();
             for (size_t k = c0; k < c1; k++) {
                 qap_rlt2 *h = pool[k - c0];
-                fac.push_back(F.fs[idx[k]]);
-                loc.push_back(F.ls[idx[k]]);
-                st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data());
-                fac.pop_back();
-                loc.pop_back();
+                if (warm) {
+                    st = qap_rlt2_fold(h, depth[F.fac.size() - base_m], F.fs[idx[k]], F.ls[idx[k]]);
+                } else {
+                    fac.push_back(F.fs[idx[k]]);
+                    loc.push_back(F.ls[idx[k]]);
+                    st = qap_rlt2_fix(h, (int)fac.size(), fac.data(), loc.data());
+                    fac.pop_back();
+                    loc.pop_back();
+                }
                 if (st != QAP_OK) return false;
                 if ((st = qap_rlt2_bound_async(h, iters, K, UB)) != QAP_OK) return false;
             }
@@ -1085,9 +1111,9 @@ struct Bnb {
             leaf(fac, loc);
             return;
         }
-        if ((st = qap_rlt2_fix(pool[0], 0, nullptr, nullptr)) != QAP_OK) return;
+        if ((st = qap_rlt2_fix(depth[0], 0, nullptr, nullptr)) != QAP_OK) return;
         qap_rlt2_result r{};
-        if ((st = qap_rlt2_bound(pool[0], iters, K, UB, &r)) != QAP_OK) return;
+        if ((st = qap_rlt2_bound(depth[0], iters, K, UB, &r)) != QAP_OK) return;
         bounded++;
         if (r.lb > UB - 1.0 + 1e-6) {
             pruned++;
@@ -1112,9 +1138,9 @@ struct Bnb {
         }
         double lb = root->lb;
         if (std::isnan(lb)) {
-            if ((st = qap_rlt2_fix(pool[0], root->m, fac.data(), loc.data())) != QAP_OK) return;
+            if ((st = qap_rlt2_fix(depth[0], root->m, fac.data(), loc.data())) != QAP_OK) return;
             qap_rlt2_result r{};
-            if ((st = qap_rlt2_bound(pool[0], iters, K, UB, &r)) != QAP_OK) return;
+            if ((st = qap_rlt2_bound(depth[0], iters, K, UB, &r)) != QAP_OK) return;
             bounded++;
             lb = r.lb;
         }
@@ -1122,6 +1148,8 @@ struct Bnb {
             pruned++;
             return;
         }
+        // warm: the given root's own state (its bound came from elsewhere): a cold bound here
+        if (warm && !std::isnan(root->lb) && !derive(0, fac, loc)) return;
         Frame F;
         if (!make_frame(fac, loc, F)) return;
         stack.push_back(std::move(F));
@@ -1197,19 +1225,62 @@ struct Bnb {
             pruned++;
             return true;
         }
+        if (warm && !derive(fac.size() - base_m, fac, loc)) return false;
         Frame F;
         if (!make_frame(fac, loc, F)) return false;
         stack.push_back(std::move(F));
         return true;
     }
+    // warm: (re)build depth[d]'s state for node (fac, loc): fold from depth[d-1] (which holds
+    // its parent) and run the node's bound again.  With K = 0 the node was bounded with all
+    // `iters` iterations when it was not pruned, so UB = +inf reproduces that state exactly.
+    // d = 0: the search root, cold (fix + bound).
+    bool derive(size_t d, const std::vector<int32_t> &fac, const std::vector<int32_t> &loc)
+    {
+        qap_rlt2_result r{};
+        if (d == 0) {
+            if ((st = qap_rlt2_fix(depth[0], (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return false;
+        } else {
+            if ((st = depth_handle(d)) != QAP_OK) return false;
+            if ((st = qap_rlt2_fold(depth[d], depth[d - 1], fac.back(), loc.back())) != QAP_OK) return false;
+        }
+        return (st = qap_rlt2_bound(depth[d], iters, K, INFINITY, &r)) == QAP_OK;
+    }
+    qap_status depth_handle(size_t d);
     ~Bnb()
     {
-        for (size_t k = 1; k < pool.size(); k++) cudaStreamSynchronize(pool[k]->stream);  // helpers: owned by h
+        for (auto x : pool) cudaStreamSynchronize(x->stream);  // helpers: owned by the caller's handle
     }
 };
 
+// depth handle d >= 1 of the warm search: owned by the caller's handle (kept across calls),
+// capacity N - d free facilities, on the caller's stream
+qap_status Bnb::depth_handle(size_t d)
+{
+    qap_rlt2 *own = depth[0];
+    while (depth.size() <= d) {
+        const size_t k = depth.size();
+        while (own->bnb_depth.size() < k) {
+            const size_t kk = own->bnb_depth.size() + 1;
+            qap_rlt2_opts op{};
+            op.device = own->device;
+            op.cuda_stream = own->stream;
+            op.flags = own->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP);
+            op.lap_warps = own->lap_warps;
+            qap_rlt2 *x = nullptr;
+            const int cap = own->N - (int)kk;
+            if (cap < 3) return fail(own, QAP_E_ARG, "warm depth beyond the last bounded level");
+            qap_status s0 = create_impl(own->N, own->F.data(), own->Dist.data(), &op, &x, false, cap);
+            if (s0 != QAP_OK) return fail(own, s0, std::string("bnb depth handle: ") + qap_last_error(nullptr));
+            own->bnb_depth.push_back(x);
+        }
+        depth.push_back(own->bnb_depth[k - 1]);
+    }
+    return QAP_OK;
+}
+
 // ---- checkpoint file (binary, little-endian; written to <path>.tmp then renamed) --------
-constexpr uint64_t kCkptMagic = 0x3154504b32544c52ull;  // "RLT2KPT1"
+constexpr uint64_t kCkptMagic = 0x3254504b32544c52ull;  // "RLT2KPT2"
 
 uint64_t instance_digest(const qap_rlt2 *h)
 {
@@ -1279,6 +1350,7 @@ bool save_checkpoint(const Bnb &B, const char *path, std::string &err)
     put(o, (int32_t)B.N);
     put(o, (int32_t)B.iters);
     put(o, (int32_t)B.sb_iters);
+    put(o, (int32_t)B.warm);
     put(o, B.K);
     put(o, B.UB0);
     put(o, B.UB);
@@ -1333,7 +1405,8 @@ bool load_checkpoint(Bnb &B, const char *path, std::string &err)
         return false;
     }
     if (R.get<uint64_t>() != instance_digest(B.h0()) || R.get<int32_t>() != B.N || R.get<int32_t>() != B.iters ||
-        R.get<int32_t>() != B.sb_iters || R.get<double>() != B.K || R.get<double>() != B.UB0) {
+        R.get<int32_t>() != B.sb_iters || R.get<int32_t>() != (int32_t)B.warm || R.get<double>() != B.K ||
+        R.get<double>() != B.UB0) {
         err = "checkpoint belongs to another instance or parameters";
         return false;
     }
@@ -1385,14 +1458,18 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
 {
     if (h->world > 1 && o->batch > 1) return fail(h, QAP_E_ARG, "batched B&B needs a single-GPU handle");
     if (o->root && !node_ok(h, o->root)) return fail(h, QAP_E_ARG, "invalid root node");
-    b.pool.push_back(h);
     b.N = h->N;
     b.iters = o->iters;
     b.K = o->K;
     b.UB = b.UB0 = o->UB0;
     b.sb_iters = o->sb_iters;
+    b.warm = o->warm != 0;
+    if (b.warm && h->world > 1) return fail(h, QAP_E_ARG, "warm B&B needs a single-GPU handle");
+    b.base_m = o->root ? o->root->m : 0;
+    b.depth.push_back(h);
     const int B = o->batch < 1 ? 1 : (o->batch > b.N ? b.N : o->batch);
-    while ((int)h->bnb_helpers.size() < B - 1) {
+    const int nh = b.warm ? B : B - 1;  // warm: the caller's handle keeps the root's state
+    while ((int)h->bnb_helpers.size() < nh) {
         cudaStream_t s = nullptr;
         cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_fail(h, e, "bnb stream");
@@ -1410,7 +1487,8 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
         h->bnb_streams.push_back(s);
         h->bnb_helpers.push_back(x);
     }
-    for (int k = 1; k < B; k++) b.pool.push_back(h->bnb_helpers[k - 1]);
+    if (!b.warm) b.pool.push_back(h);
+    for (int k = 0; k < nh; k++) b.pool.push_back(h->bnb_helpers[k]);
     return QAP_OK;
 }
 
@@ -1443,6 +1521,10 @@ qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
     std::string err;
     if (o->resume) {
         if (!load_checkpoint(b, o->checkpoint_path, err)) return fail(h, QAP_E_ARG, err);
+        // warm: the device states of the expanded nodes on the DFS path are rebuilt
+        if (b.warm)
+            for (size_t k = 0; k < b.stack.size(); k++)
+                if (!b.derive(k, b.stack[k].fac, b.stack[k].loc)) return b.st;
     } else {
         b.start_at(o->root);
         if (b.st != QAP_OK) return b.st;
@@ -1477,7 +1559,9 @@ qap_status qap_bnb_frontier(qap_rlt2 *h, const qap_bnb_opts *o, int32_t target, 
 {
     if (!h || !o || !out || !n_nodes || o->iters < 0 || cap < 0 || (cap > 0 && !nodes)) return QAP_E_ARG;
     Bnb b;
-    qap_status st0 = bnb_init(h, o, b);
+    qap_bnb_opts oc = *o;
+    oc.warm = 0;  // the breadth-first frontier bounds cold (node states are not kept level-wide)
+    qap_status st0 = bnb_init(h, &oc, b);
     if (st0 != QAP_OK) return st0;
     qap_bnb_node root{};
     root.lb = NAN;

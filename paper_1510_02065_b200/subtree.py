@@ -135,21 +135,23 @@ def run_worker(q: SubtreeQueue, frontier: list, solve, sync_every: int = 32) -> 
     return tot
 
 
-def gpu_solver(pkg, h, iters: int, K: float = 0.0, batch: int = 1, sb_iters: int = -1, sync_every: int = 32):
+def gpu_solver(pkg, h, iters: int, K: float = 0.0, batch: int = 1, sb_iters: int = -1, sync_every: int = 32,
+               warm: bool = False):
     """solve() for run_worker on a single-GPU handle h (qap_bnb_run with the hooks)."""
     def solve(node, ub0, sync, donate):
         return pkg.qap_bnb_run(h, iters, K=K, UB0=ub0, batch=batch, sb_iters=sb_iters, root=node, sync=sync,
-                               donate=donate, sync_every=sync_every)
+                               donate=donate, sync_every=sync_every, warm=warm)
     return solve
 
 
 def subtree_bnb(pkg, h, store, rank: int, world: int, iters: int, target: int | None = None, K: float = 0.0,
                 batch: int = 1, sb_iters: int = -1, sync_every: int = 32, prefix: str = "bnb/",
-                frontier_handle=None) -> dict:
+                frontier_handle=None, warm: bool = False) -> dict:
     """Subtree-parallel B&B with one worker per (rank, handle h).  Every worker calls this.
     frontier_handle: handle for phase 1 (e.g. a sharded group handle; default h, each worker
-    computing the identical frontier).  Returns the global optimum, a permutation of it and
-    the summed counters (frontier counted once)."""
+    computing the identical frontier).  warm: warm children below each task's root (the task
+    root itself is re-bounded cold on its worker).  Returns the global optimum, a permutation
+    of it and the summed counters (frontier counted once)."""
     fh = frontier_handle if frontier_handle is not None else h
     fbatch = batch if getattr(fh, "world", 1) <= 1 else 1
     target = target if target is not None else 4 * world
@@ -157,7 +159,7 @@ def subtree_bnb(pkg, h, store, rank: int, world: int, iters: int, target: int | 
     q = SubtreeQueue(store, rank, world, len(nodes), ub0=fr["opt"], prefix=prefix)
     if fr["opt"] >= 0:
         q.publish(fr["opt"], fr["perm"])
-    mine = run_worker(q, nodes, gpu_solver(pkg, h, iters, K, batch, sb_iters, sync_every), sync_every)
+    mine = run_worker(q, nodes, gpu_solver(pkg, h, iters, K, batch, sb_iters, sync_every, warm), sync_every)
     stats = q.gather_stats(mine)
     opt, perm = q.solution()
     out = dict(opt=opt, perm=perm, frontier_nodes=len(nodes), workers=stats)

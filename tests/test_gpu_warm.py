@@ -106,3 +106,67 @@ def test_fold_errors(pkg):
         pkg.qap_rlt2_fold(h4c, h4, 1, 1)         # child of size 2: a leaf
     for x in (hp, hc, ho, h4, h4c):
         pkg.qap_destroy(x)
+
+
+@pytest.mark.parametrize("batch", [1, 4, 16])
+@pytest.mark.parametrize("family,n,sb", [("nug", 7, -1), ("taib", 8, -1), ("uniform", 8, -1), ("nug", 10, -1),
+                                         ("nug", 9, 1), ("taib", 9, 1)])
+def test_warm_bnb_parity(orc, pkg, family, n, sb, batch):
+    """Warm B&B: node counts, optimum and permutation identical to the oracle's warm B&B
+    (one node at a time) also with children bounded concurrently; optimum = brute force."""
+    from tests import dualeval as de
+    inst = qapgen.make(family, n, 1)
+    h = pkg.qap_rlt2_create(n, inst.F, inst.D)
+    g = pkg.qap_bnb_solve(h, 2, batch=batch, sb_iters=sb, warm=True)
+    o = orc.bnb(inst.F, inst.D, T=2, sb_iters=sb, warm=True)
+    assert g["opt"] == o["opt"]
+    assert (g["perm"] == o["perm"]).all()
+    assert (g["bounded"], g["leaves"], g["pruned"], g["sb_cut"]) == (o["bounded"], o["leaves"], o["pruned"],
+                                                                     o["sb_cut"])
+    if n <= 9:
+        assert g["opt"] == de.brute_force_opt(inst.F, inst.D)
+    # cold search on the same handle afterwards is unaffected
+    c = pkg.qap_bnb_solve(h, 2, batch=batch, sb_iters=sb)
+    oc = orc.bnb(inst.F, inst.D, T=2, sb_iters=sb)
+    assert (c["bounded"], c["opt"]) == (oc["bounded"], oc["opt"])
+    pkg.qap_destroy(h)
+
+
+def test_warm_bnb_checkpoint_resume(orc, pkg, tmp_path):
+    inst = qapgen.nug(10, 2)
+    h = pkg.qap_rlt2_create(10, inst.F, inst.D)
+    ref = pkg.qap_bnb_run(h, 2, batch=4, warm=True)
+    path = str(tmp_path / "warm.ckpt")
+    r = pkg.qap_bnb_run(h, 2, batch=4, warm=True, checkpoint_path=path, max_nodes=9)
+    assert not r["complete"]
+    while not r["complete"]:
+        r = pkg.qap_bnb_run(h, 2, batch=3, warm=True, checkpoint_path=path, max_nodes=7, resume=True)
+    assert (r["opt"], r["bounded"], r["leaves"], r["pruned"]) == (ref["opt"], ref["bounded"], ref["leaves"],
+                                                                   ref["pruned"])
+    with pytest.raises(pkg.QapError):  # a cold run cannot resume a warm checkpoint
+        pkg.qap_bnb_run(h, 2, batch=4, checkpoint_path=path, resume=True)
+    pkg.qap_destroy(h)
+
+
+def test_warm_subtree_workers(orc, torch, pkg):
+    import threading
+    import torch.distributed as dist
+    from paper_1510_02065_b200 import subtree
+    from tests import dualeval as de
+    inst = qapgen.taib(9, 3)
+    store = dist.HashStore()
+    hs = [pkg.qap_rlt2_create(9, inst.F, inst.D, stream=torch.cuda.Stream().cuda_stream) for _ in range(2)]
+    out = [None, None]
+
+    def body(r):
+        out[r] = subtree.subtree_bnb(pkg, hs[r], store, r, 2, 2, target=1, batch=3, sync_every=1, warm=True,
+                                     prefix="warm/")
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(2)]
+    [t.start() for t in th]
+    [t.join(300) for t in th]
+    opt = de.brute_force_opt(inst.F, inst.D)
+    assert out[0]["opt"] == out[1]["opt"] == opt
+    assert inst.evaluate(out[0]["perm"]) == opt
+    for x in hs:
+        pkg.qap_destroy(x)
