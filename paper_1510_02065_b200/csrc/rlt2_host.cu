@@ -959,6 +959,7 @@ struct Frame {
     std::vector<double> est, lb;    // RLT1 estimate (-inf without strong branching), RLT2 bound
     uint32_t next = 0;
     uint8_t child_leaf = 0;
+    uint64_t id = 0;  // warm: identifies the frame whose children the pool handles hold
 };
 
 struct Bnb {
@@ -968,6 +969,11 @@ struct Bnb {
     bool warm = false;
     int base_m = 0;
     std::vector<qap_rlt2 *> depth;
+    // warm: pool handle j holds the post-bound state of child holds[j].second of the frame
+    // with id holds[j].first (until the handle is reused): expanding that child copies it
+    uint64_t next_id = 1;
+    std::vector<std::pair<uint64_t, int>> holds;
+    int64_t copies = 0, rederived = 0;
     int N = 0, iters = 0, sb_iters = -1;
     double K = 0.0, UB = INFINITY, UB0 = INFINITY;
     bool have = false;
@@ -1059,6 +1065,7 @@ struct Bnb {
                 }
                 if (st != QAP_OK) return false;
                 if ((st = qap_rlt2_bound_async(h, iters, K, UB)) != QAP_OK) return false;
+                if (warm) holds[k - c0] = {F.id, (int)idx[k]};
             }
             for (size_t k = c0; k < c1; k++) {
                 qap_rlt2_result r{};
@@ -1076,7 +1083,9 @@ struct Bnb {
         std::vector<int> ffac, floc;
         free_sets(fac, loc, ffac, floc);
         const int n = (int)ffac.size();
+        F.id = next_id++;
         if (sb_iters >= 0 && n >= 5) {  // strong branching
+            if (warm) holds[0] = {0, -1};
             if ((st = qap_rlt2_fix(pool[0], (int)fac.size(), fac.data(), loc.data())) != QAP_OK) return false;
             std::vector<double> e((size_t)n * n);
             int32_t kind = 0, index = 0;
@@ -1225,7 +1234,20 @@ struct Bnb {
             pruned++;
             return true;
         }
-        if (warm && !derive(fac.size() - base_m, fac, loc)) return false;
+        if (warm) {
+            const size_t d = fac.size() - base_m;
+            int j = -1;
+            for (size_t q = 0; q < holds.size(); q++)
+                if (holds[q].first == T.id && holds[q].second == (int)c) j = (int)q;
+            if (j >= 0) {
+                if ((st = depth_handle(d)) != QAP_OK) return false;
+                if ((st = copy_state(depth[d], pool[j])) != QAP_OK) return false;
+                copies++;
+            } else {
+                if (!derive(d, fac, loc)) return false;
+                rederived++;
+            }
+        }
         Frame F;
         if (!make_frame(fac, loc, F)) return false;
         stack.push_back(std::move(F));
@@ -1247,6 +1269,7 @@ struct Bnb {
         return (st = qap_rlt2_bound(depth[d], iters, K, INFINITY, &r)) == QAP_OK;
     }
     qap_status depth_handle(size_t d);
+    static qap_status copy_state(qap_rlt2 *dst, const qap_rlt2 *src);
     ~Bnb()
     {
         for (auto x : pool) cudaStreamSynchronize(x->stream);  // helpers: owned by the caller's handle
@@ -1276,6 +1299,38 @@ qap_status Bnb::depth_handle(size_t d)
         }
         depth.push_back(own->bnb_depth[k - 1]);
     }
+    return QAP_OK;
+}
+
+// dst := src's node and dual state (same instance, single GPU, src at an iteration
+// boundary), ordered after src's pending work; device-to-device copies on dst's stream
+qap_status Bnb::copy_state(qap_rlt2 *dst, const qap_rlt2 *src)
+{
+    const Geom &g = src->geom;
+    if (g.n > dst->n_cap) return fail(dst, QAP_E_CAPACITY, "state copy: node larger than the target");
+    cudaError_t e;
+    if ((e = cudaEventRecord(src->evJoin, src->stream)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(dst->stream, src->evJoin, 0)) != cudaSuccess)
+        return cuda_fail(dst, e, "state copy ordering");
+    const size_t nb = (size_t)g.n * g.n * 8, nc = (size_t)g.n * g.n * g.ldc * 8, nd = (size_t)g.nblk * g.ld2 * 8;
+    if ((e = cudaMemcpyAsync(dst->dB, src->dB, nb, cudaMemcpyDeviceToDevice, dst->stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dst->dC, src->dC, nc, cudaMemcpyDeviceToDevice, dst->stream)) != cudaSuccess ||
+        (!src->d_zero &&
+         (e = cudaMemcpyAsync(dst->dD, src->dD, nd, cudaMemcpyDeviceToDevice, dst->stream)) != cudaSuccess) ||
+        (e = cudaMemcpyAsync(dst->dCtl, src->dCtl, sizeof(Ctl), cudaMemcpyDeviceToDevice, dst->stream)) !=
+            cudaSuccess ||
+        (e = cudaMemcpyAsync(dst->dTriples, src->dTriples, (size_t)g.n * (g.n - 1) * (g.n - 2) / 6 * sizeof(int),
+                             cudaMemcpyDeviceToDevice, dst->stream)) != cudaSuccess)
+        return cuda_fail(dst, e, "state copy");
+    if ((e = cudaEventRecord(dst->evJoin, dst->stream)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(src->stream, dst->evJoin, 0)) != cudaSuccess)
+        return cuda_fail(dst, e, "state copy ordering");
+    dst->node = src->node;
+    dst->geom = src->geom;
+    dst->next_phase = src->next_phase;
+    dst->d_zero = src->d_zero;
+    dst->b_zero = src->b_zero;
+    dst->c_zero = src->c_zero;
     return QAP_OK;
 }
 
@@ -1489,6 +1544,7 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
     }
     if (!b.warm) b.pool.push_back(h);
     for (int k = 0; k < nh; k++) b.pool.push_back(h->bnb_helpers[k]);
+    b.holds.assign(b.pool.size(), {0, -1});
     return QAP_OK;
 }
 
