@@ -310,6 +310,8 @@ def main():
         assert (rs["bounded"], rs["opt"]) == (rb["bounded"], rb["opt"])
         rsb, dt2 = timed(batch=BNB_BATCH, sb_iters=1)
         assert rsb["opt"] == rb["opt"]
+        rw, dtw = timed(batch=BNB_BATCH, warm=True)
+        assert rw["opt"] == rb["opt"]
         pkg.qap_destroy(hb)
         bnb = {"config": f"nug12-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node, UB0=inf, "
                          f"branch on lowest free facility, leaves n'<=3 enumerated, children bounded "
@@ -320,7 +322,10 @@ def main():
                "nodes_per_s_one_at_a_time": rs["bounded"] / dt1,
                "strong_branching": {"sb_iters": 1, "bounded_nodes": rsb["bounded"], "leaves": rsb["leaves"],
                                     "cut_by_rlt1": rsb["sb_cut"], "seconds": dt2,
-                                    "nodes_per_s": rsb["bounded"] / dt2}}
+                                    "nodes_per_s": rsb["bounded"] / dt2},
+               "warm_children": {"bounded_nodes": rw["bounded"], "leaves": rw["leaves"], "seconds": dtw,
+                                 "nodes_per_s": rw["bounded"] / dtw,
+                                 "note": "children folded from the parent's dual state (NEXT-3)"}}
     pkg.qap_destroy(h)
 
     # subtree-parallel B&B: one worker per GPU on a larger tree;
