@@ -67,6 +67,7 @@ typedef struct {
 #define QAP_FLAG_OVERLAP 2        /* run the D transfer and the level-2 LAPs concurrently on two
                                      internal streams (experimental; default: one after the other) */
 #define QAP_FLAG_NO_GRAPH 4       /* do not replay the iteration loop from a cached CUDA graph     */
+#define QAP_FLAG_LDG_TRANSFER 8   /* transfer with per-element loads instead of tensor-map TMA    */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */

@@ -5,11 +5,13 @@
 // The stop test is evaluated on the device after each iteration and turns
 // the remaining launches of the call into no-ops, so a bound call synchronises once.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -84,6 +86,9 @@ struct qap_rlt2 {
     // the current DFS path (capacity N - d, on this handle's stream)
     std::vector<qap_rlt2 *> bnb_depth;
     int n_cap = 0;  // largest node (free facilities) the buffers hold
+    // tensor maps of D for k_transfer_tma, encoded for node size tma_n (0: none / failed)
+    TmaMaps tma{};
+    int tma_n = 0;
 };
 
 static std::string g_create_error;
@@ -560,6 +565,47 @@ static cudaError_t run_shard_sub(qap_rlt2 *h, int phase, int sub, cudaStream_t s
     return e;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder()
+{
+    static std::once_flag once;
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// tensor maps of the current node's stored blocks (one per first facility f): the blocks of
+// f as [j][k - f - 1][l'][entry], strides in bytes; false: use the per-element-load kernel
+static bool tma_maps(qap_rlt2 *h)
+{
+    const Geom &g = h->geom;
+    if (h->world > 1 || h->loopback) return false;
+    if (h->tma_n == g.n) return true;
+    if (h->tma_n == -g.n) return false;  // encoding failed for this size before
+    auto enc = tma_encoder();
+    const int n = g.n, n1 = n - 1;
+    // every box extent within the tensor's: kBox1 <= n - 1, TT <= n (and kBox0 <= ld2)
+    bool ok = enc != nullptr && n - 1 >= kBox1 && n >= TT && g.ld2 >= kBox0;
+    for (int f = 0; ok && f + 1 < n; f++) {
+        const cuuint64_t ld = (cuuint64_t)g.ld2;
+        cuuint64_t dims[4] = {ld, (cuuint64_t)n1, (cuuint64_t)(n1 - f), (cuuint64_t)n};
+        cuuint64_t strides[3] = {ld * 8, (cuuint64_t)n1 * ld * 8, (cuuint64_t)(n1 - f) * n1 * ld * 8};
+        cuuint32_t box[4] = {(cuuint32_t)tma_box0(n), (cuuint32_t)kBox1, 1u, (cuuint32_t)TT};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        ok = enc(&h->tma.m[f], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dD + g.off[f] * g.ld2, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    h->tma_n = ok ? n : -n;
+    return ok;
+}
+
 static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused)
 {
     cudaError_t e = cudaSuccess;
@@ -607,7 +653,10 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
                 if ((e = cudaStreamWaitEvent(sL, h->evS, 0)) != cudaSuccess) return e;
             }
             const TransferArgs A = transfer_args(h, ov ? 1 : 0);
-            e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) { return launch_transfer(A, 0, s); });
+            const bool tma = !ov && !(h->flags & QAP_FLAG_LDG_TRANSFER) && tma_maps(h);
+            e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {
+                return tma ? launch_transfer_tma(A, h->tma, s) : launch_transfer(A, 0, s);
+            });
             if (e) return e;
             h->d_zero = 0;
             h->b_zero = h->c_zero = 1;

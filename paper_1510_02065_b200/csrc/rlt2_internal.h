@@ -1,6 +1,7 @@
 // rlt2_internal.h — device-state layout and kernel launchers shared by the CUDA kernels
 // (rlt2_kernels.cu) and the host control (rlt2_host.cu).  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -129,6 +130,14 @@ struct TransferArgs {
     int pack;             // 1: write this side's partial of AGG/HOLD tiles; 0: apply
 };
 cudaError_t launch_transfer(const TransferArgs &A, int ntiles_list, cudaStream_t st);
+// tensor maps of the stored blocks, one per first facility (k_transfer_tma); box extents
+constexpr int kBox0 = TT + 4, kBox1 = TT + 1;  // dim0: TT+2 columns + an even (16-byte) start
+// (dim0 = in-block entries, dim1 = second location, dim2 = 1 second facility, dim3 = TT first locations)
+struct TmaMaps {
+    CUtensorMap m[kMaxN];
+};
+cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStream_t st);
+int tma_box0(int n);  // dim0 box extent for node size n (TT + 2 when n - 2 is even, else TT + 4)
 struct Offsets {
     int64_t off[kMaxN];
 };

@@ -15,6 +15,7 @@
 // Arithmetic order follows DESIGN.md §3 exactly (same IEEE operations as the paper's
 // algorithm written out), so results are reproducible bit for bit; no multiplies
 // occur in fp64 after initialisation (compiled with -fmad=false regardless).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -57,6 +58,16 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+// 4-D tensor-map TMA load of one box (coordinates in elements, dim0 innermost)
+__device__ __forceinline__ void tma_load_4d(void *dst, const void *tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t *mbar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(mbar))
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity)
@@ -982,6 +993,137 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
 }
 
 // ---------------------------------------------------------------------------------------
+// k_transfer_tma — the same transfer (identical operations per class, reading R11) with the
+// three member views of a tile fetched by tensor-map TMA instead of per-element loads.  Per
+// first facility f a 4-D tensor map views the stored blocks of f as
+//   [j (first location)][k - f - 1 (second facility)][l' (second location, skip-indexed)]
+//   [in-block entry]
+// (TmaMaps, encoded on the host per node size).  A tile's view is one box of
+// TT (j) x 1 x (TT+1) (l') x (TT+4) (entries): the row of the third facility with a window of
+// TT+2 columns — wide enough for the skip-indexed positions of every (j, l, q) of the tile —
+// started at an even entry (TMA needs 16-byte aligned box starts in the innermost dimension).
+// Boxes overlap neighbouring tiles, so results are stored element-wise (coalesced runs of
+// <= 8 doubles per view row), only for the tile's own classes.  Unsharded handles only.
+// ---------------------------------------------------------------------------------------
+constexpr int BX1 = kBox1;
+
+// position in view vw's box of the element of class (j,l,q) (tile origin j0, l0, q0).
+// The box's dim0 window starts at the even entry at or below (row * m2 + w): TMA needs a
+// 16-byte aligned start in the innermost dimension; odd = 1 when it was moved down by one.
+template <int BX0>
+__device__ __forceinline__ int box_pos(int vw, int j, int l, int q, int j0, int l0, int q0, int odd)
+{
+    if (vw == 0) {  // D{ij,kl}[p-2][q'] : rows (j, l'), column q'
+        const int lp = l - (l > j), qp = q - (q > j) - (q > l);
+        const int ls = l0 > 0 ? l0 - 1 : 0, w = q0 > 1 ? q0 - 2 : 0;
+        return ((j - j0) * BX1 + (lp - ls)) * BX0 + (qp - w + odd);
+    } else if (vw == 1) {  // D{ij,pq}[k-1][l'] : rows (j, q'), column l'
+        const int qp = q - (q > j), lp = l - (l > j) - (l > q);
+        const int qs = q0 > 0 ? q0 - 1 : 0, w = l0 > 1 ? l0 - 2 : 0;
+        return ((j - j0) * BX1 + (qp - qs)) * BX0 + (lp - w + odd);
+    } else {  // D{kl,pq}[i][j'] : rows (l, q'), column j'
+        const int qp = q - (q > l), jp = j - (j > l) - (j > q);
+        const int qs = q0 > 0 ? q0 - 1 : 0, w = j0 > 1 ? j0 - 2 : 0;
+        return ((l - l0) * BX1 + (qp - qs)) * BX0 + (jp - w + odd);
+    }
+}
+
+template <int BX0>  // TT + 2 (m2 even: window starts are even) or TT + 4
+__global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, const __grid_constant__ TmaMaps M)
+{
+    constexpr int BOXE = TT * BX1 * BX0;
+    if (A.ctl->stopped) return;
+    __shared__ __align__(128) double box[3][BOXE];
+    __shared__ unsigned rbase[3][TT * TT];
+    __shared__ double rsig[3][TT * TT];
+    __shared__ __align__(8) uint64_t mbar;
+    const Geom &g = A.g;
+    const int n = g.n, m2 = n - 2, ntile = A.ntile;
+    const int64_t ld2 = g.ld2;
+    const int tri = A.triples[blockIdx.y];
+    const int i = tri & 0xff, k = (tri >> 8) & 0xff, p = tri >> 16;
+    const int tile = blockIdx.x, tl = tile / ntile, tj = tl / ntile;
+    const int q0 = (tile - tl * ntile) * TT, l0 = (tl - tj * ntile) * TT, j0 = tj * TT;
+    const int tid = threadIdx.x;
+    const bool dz = A.d_zero != 0;
+    // dim0 window starts (entries) of the three views, before rounding down to even
+    const int s0 = (p - 2) * m2 + (q0 > 1 ? q0 - 2 : 0), s1 = (k - 1) * m2 + (l0 > 1 ? l0 - 2 : 0),
+              s2 = i * m2 + (j0 > 1 ? j0 - 2 : 0);
+    const int o0 = s0 & 1, o1 = s1 & 1, o2 = s2 & 1;
+    if (tid == 0 && !dz) {
+        mbar_init(&mbar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&mbar, 3u * BOXE * 8u);
+        tma_load_4d(box[0], &M.m[i], s0 - o0, l0 > 0 ? l0 - 1 : 0, k - i - 1, j0, &mbar);
+        tma_load_4d(box[1], &M.m[i], s1 - o1, q0 > 0 ? q0 - 1 : 0, p - i - 1, j0, &mbar);
+        tma_load_4d(box[2], &M.m[k], s2 - o2, q0 > 0 ? q0 - 1 : 0, p - k - 1, l0, &mbar);
+    }
+    // per view row: element index of the row in D (stores) and sigma of its block
+    if (tid < 3 * TT * TT) {
+        const int vw = tid >> 6, x = (tid >> 3) & 7, y = tid & 7;
+        int r0, r1;
+        if (vw == 0) { r0 = j0 + x; r1 = l0 + y; }
+        else if (vw == 1) { r0 = j0 + x; r1 = q0 + y; }
+        else { r0 = l0 + x; r1 = q0 + y; }
+        unsigned base = NOIDX;
+        double sg = 0.0;
+        if (r0 < n && r1 < n && r0 != r1) {
+            int64_t bb;
+            int row;
+            if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; }
+            else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; }
+            else { bb = bid_of(g, k, r0, p, r1); row = i; }
+            sg = A.sigma[bb];
+            base = (unsigned)(bb * ld2 + row * m2);
+        }
+        rbase[vw][tid & 63] = base;
+        rsig[vw][tid & 63] = sg;
+    }
+    __syncthreads();
+    if (!dz) mbar_wait(&mbar, 0);
+    // mean of each class (j,l,q) of the tile: ((e1 + e2) + e3) / 3 with e = stored + sigma
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int e = tid + 256 * h;
+        const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;
+        const int j = j0 + a, l = l0 + b, q = q0 + c;
+        if (j < n && l < n && q < n && j != l && j != q && l != q) {
+            const int p0 = box_pos<BX0>(0, j, l, q, j0, l0, q0, o0), p1 = box_pos<BX0>(1, j, l, q, j0, l0, q0, o1),
+                      p2 = box_pos<BX0>(2, j, l, q, j0, l0, q0, o2);
+            const double e1 = (dz ? 0.0 : box[0][p0]) + rsig[0][a * 8 + b];
+            const double e2 = (dz ? 0.0 : box[1][p1]) + rsig[1][a * 8 + c];
+            const double e3 = (dz ? 0.0 : box[2][p2]) + rsig[2][b * 8 + c];
+            const double mu = ((e1 + e2) + e3) / 3.0;
+            box[0][p0] = mu;
+            box[1][p1] = mu;
+            box[2][p2] = mu;
+        }
+    }
+    __syncthreads();
+    // store each view's own elements: element (x,y,z) = row (x,y), free index z (contiguous)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int e = tid + 256 * h;
+        const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
+#pragma unroll
+        for (int vw = 0; vw < 3; vw++) {
+            const int a = (vw == 2 ? l0 : j0) + x;               // the row's two locations
+            const int b = (vw == 0 ? l0 : q0) + y;
+            const int f = (vw == 0 ? q0 : (vw == 1 ? l0 : j0)) + z;  // the free (column) location
+            const unsigned base = rbase[vw][e >> 3];
+            if (base != NOIDX && f < n && f != a && f != b) {
+                int j, l, q;
+                if (vw == 0) { j = a; l = b; q = f; }
+                else if (vw == 1) { j = a; q = b; l = f; }
+                else { l = a; q = b; j = f; }
+                A.D[base + (unsigned)(f - (f > a) - (f > b))] =
+                    box[vw][box_pos<BX0>(vw, j, l, q, j0, l0, q0, vw == 0 ? o0 : (vw == 1 ? o1 : o2))];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Strong branching: RLT1 bounds of the n^2 candidate children of a node at once.
 // Child c = a * n + b fixes free facility I[a] at free location J[b] in addition to the
 // node's pairs; its reduced costs are built as in k_init (O0/O1).
@@ -1111,6 +1253,18 @@ cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double
     int blocks = (int)((tot + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_sigma<<<blocks, 256, 0, st>>>(g, B, C, sigma, ctl, sched);
+    return cudaGetLastError();
+}
+
+int tma_box0(int n) { return ((n - 2) & 1) ? kBox0 : kBox0 - 2; }
+
+cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStream_t st)
+{
+    const int n = A.g.n;
+    const int ntri = n * (n - 1) * (n - 2) / 6;
+    dim3 grid(A.ntile * A.ntile * A.ntile, ntri);
+    if (tma_box0(n) == kBox0) k_transfer_tma<kBox0><<<grid, 256, 0, st>>>(A, M);
+    else k_transfer_tma<kBox0 - 2><<<grid, 256, 0, st>>>(A, M);
     return cudaGetLastError();
 }
 

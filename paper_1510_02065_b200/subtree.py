@@ -46,6 +46,10 @@ class SubtreeQueue:
             self.s.add(self.p + "alloc", n_frontier)
             self.s.set(self.p + "ready", "1")
         self.s.wait([self.p + "ready"])
+        # start barrier: every worker registered before tasks are taken (donation requests see them)
+        self.s.add(self.p + "arrived", 1)
+        while self._get("arrived") < world:
+            time.sleep(0.0005)
 
     # -- counters -----------------------------------------------------------------------
     def _get(self, k: str) -> int:

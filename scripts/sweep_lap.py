@@ -8,7 +8,7 @@ import qapgen
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 # (flags, lap_cfg)
-cfgs = [(0, 0x20)]
+cfgs = [(0, 0x20), (8, 0x20)] if len(sys.argv) < 3 else [(int(x, 0), 0x20) for x in sys.argv[2].split(",")]
 torch.cuda.set_device(0)
 inst = qapgen.nug(n, 1)
 ref = None
