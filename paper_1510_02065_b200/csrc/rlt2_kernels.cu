@@ -1034,6 +1034,7 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
     constexpr int BOXE = TT * BX1 * BX0;
     if (A.ctl->stopped) return;
     __shared__ __align__(128) double box[3][BOXE];
+    __shared__ double mean[TT * TT * TT];  // class (a,b,c) = (j-j0, l-l0, q-q0) -> its mean
     __shared__ unsigned rbase[3][TT * TT];
     __shared__ double rsig[3][TT * TT];
     __shared__ __align__(8) uint64_t mbar;
@@ -1081,44 +1082,39 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
     }
     __syncthreads();
     if (!dz) mbar_wait(&mbar, 0);
-    // mean of each class (j,l,q) of the tile: ((e1 + e2) + e3) / 3 with e = stored + sigma
+    // mean of each class (j,l,q) of the tile: ((e1 + e2) + e3) / 3 with e = stored + sigma.
+    // View 0's store element e is class e itself: stored from the register right away.
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int e = tid + 256 * h;
         const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;
         const int j = j0 + a, l = l0 + b, q = q0 + c;
         if (j < n && l < n && q < n && j != l && j != q && l != q) {
-            const int p0 = box_pos<BX0>(0, j, l, q, j0, l0, q0, o0), p1 = box_pos<BX0>(1, j, l, q, j0, l0, q0, o1),
-                      p2 = box_pos<BX0>(2, j, l, q, j0, l0, q0, o2);
-            const double e1 = (dz ? 0.0 : box[0][p0]) + rsig[0][a * 8 + b];
-            const double e2 = (dz ? 0.0 : box[1][p1]) + rsig[1][a * 8 + c];
-            const double e3 = (dz ? 0.0 : box[2][p2]) + rsig[2][b * 8 + c];
+            const double e1 = (dz ? 0.0 : box[0][box_pos<BX0>(0, j, l, q, j0, l0, q0, o0)]) + rsig[0][a * 8 + b];
+            const double e2 = (dz ? 0.0 : box[1][box_pos<BX0>(1, j, l, q, j0, l0, q0, o1)]) + rsig[1][a * 8 + c];
+            const double e3 = (dz ? 0.0 : box[2][box_pos<BX0>(2, j, l, q, j0, l0, q0, o2)]) + rsig[2][b * 8 + c];
             const double mu = ((e1 + e2) + e3) / 3.0;
-            box[0][p0] = mu;
-            box[1][p1] = mu;
-            box[2][p2] = mu;
+            mean[e] = mu;
+            A.D[rbase[0][e >> 3] + (unsigned)(q - (q > j) - (q > l))] = mu;  // row (j,l), column q'
         }
     }
     __syncthreads();
-    // store each view's own elements: element (x,y,z) = row (x,y), free index z (contiguous)
+    // views 1 and 2: element (x,y,z) = row (x,y), free index z (contiguous runs in D)
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int e = tid + 256 * h;
         const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
-#pragma unroll
-        for (int vw = 0; vw < 3; vw++) {
-            const int a = (vw == 2 ? l0 : j0) + x;               // the row's two locations
-            const int b = (vw == 0 ? l0 : q0) + y;
-            const int f = (vw == 0 ? q0 : (vw == 1 ? l0 : j0)) + z;  // the free (column) location
-            const unsigned base = rbase[vw][e >> 3];
-            if (base != NOIDX && f < n && f != a && f != b) {
-                int j, l, q;
-                if (vw == 0) { j = a; l = b; q = f; }
-                else if (vw == 1) { j = a; q = b; l = f; }
-                else { l = a; q = b; j = f; }
-                A.D[base + (unsigned)(f - (f > a) - (f > b))] =
-                    box[vw][box_pos<BX0>(vw, j, l, q, j0, l0, q0, vw == 0 ? o0 : (vw == 1 ? o1 : o2))];
-            }
+        {   // view 1: row (j, q) = (j0 + x, q0 + y), free l = l0 + z; class (x, z, y)
+            const int a = j0 + x, b = q0 + y, f = l0 + z;
+            const unsigned base = rbase[1][e >> 3];
+            if (base != NOIDX && f < n && f != a && f != b)
+                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[x * 64 + z * 8 + y];
+        }
+        {   // view 2: row (l, q) = (l0 + x, q0 + y), free j = j0 + z; class (z, x, y)
+            const int a = l0 + x, b = q0 + y, f = j0 + z;
+            const unsigned base = rbase[2][e >> 3];
+            if (base != NOIDX && f < n && f != a && f != b)
+                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[z * 64 + x * 8 + y];
         }
     }
 }
