@@ -382,7 +382,10 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
             for (int r = 0; r < m; r++) {
                 const double x = (Mc[r * m] - urow[r]) - vc;
                 neg |= x < -1e-9;
-                Mc[r * m] = x > 0.0 ? x : 0.0;  // x <= 0 (incl. -0) -> +0
+                // x <= 0 (incl. -0) -> +0, else x (== x > 0.0 ? x : 0.0 for every non-NaN x):
+                // clear both words when the sign bit is set
+                const int hi = __double2hiint(x), lo = __double2loint(x), keep = ~(hi >> 31);
+                Mc[r * m] = __hiloint2double(hi & keep, lo & keep);
             }
             Mc[p[t] * m] = 0.0;  // assigned cell -> +0
         }
@@ -1005,8 +1008,6 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
 // Boxes overlap neighbouring tiles, so results are stored element-wise (coalesced runs of
 // <= 8 doubles per view row), only for the tile's own classes.  Unsharded handles only.
 // ---------------------------------------------------------------------------------------
-constexpr int BX1 = kBox1;
-
 // position in view vw's box of the element of class (j,l,q) (tile origin j0, l0, q0).
 // The box's dim0 window starts at the even entry at or below (row * m2 + w): TMA needs a
 // 16-byte aligned start in the innermost dimension; odd = 1 when it was moved down by one.
@@ -1016,25 +1017,28 @@ __device__ __forceinline__ int box_pos(int vw, int j, int l, int q, int j0, int 
     if (vw == 0) {  // D{ij,kl}[p-2][q'] : rows (j, l'), column q'
         const int lp = l - (l > j), qp = q - (q > j) - (q > l);
         const int ls = l0 > 0 ? l0 - 1 : 0, w = q0 > 1 ? q0 - 2 : 0;
-        return ((j - j0) * BX1 + (lp - ls)) * BX0 + (qp - w + odd);
+        return ((j - j0) * kBox1 + (lp - ls)) * BX0 + (qp - w + odd);
     } else if (vw == 1) {  // D{ij,pq}[k-1][l'] : rows (j, q'), column l'
         const int qp = q - (q > j), lp = l - (l > j) - (l > q);
         const int qs = q0 > 0 ? q0 - 1 : 0, w = l0 > 1 ? l0 - 2 : 0;
-        return ((j - j0) * BX1 + (qp - qs)) * BX0 + (lp - w + odd);
+        return ((j - j0) * kBox1 + (qp - qs)) * BX0 + (lp - w + odd);
     } else {  // D{kl,pq}[i][j'] : rows (l, q'), column j'
         const int qp = q - (q > l), jp = j - (j > l) - (j > q);
         const int qs = q0 > 0 ? q0 - 1 : 0, w = j0 > 1 ? j0 - 2 : 0;
-        return ((l - l0) * BX1 + (qp - qs)) * BX0 + (jp - w + odd);
+        return ((l - l0) * kBox1 + (qp - qs)) * BX0 + (jp - w + odd);
     }
 }
 
 template <int BX0>  // TT + 2 (m2 even: window starts are even) or TT + 4
 __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, const __grid_constant__ TmaMaps M)
 {
-    constexpr int BOXE = TT * BX1 * BX0;
+    constexpr int BOXE = TT * kBox1 * BX0;
     if (A.ctl->stopped) return;
     __shared__ __align__(128) double box[3][BOXE];
-    __shared__ double mean[TT * TT * TT];  // class (a,b,c) = (j-j0, l-l0, q-q0) -> its mean
+    // class (a,b,c) = (j-j0, l-l0, q-q0) -> its mean at a * MA + b * MB + c (odd strides:
+    // the permuted reads of the store phase are bank-conflict free)
+    constexpr int MB = TT + 1, MA = TT * MB + 1;
+    __shared__ double mean[TT * MA];
     __shared__ unsigned rbase[3][TT * TT];
     __shared__ double rsig[3][TT * TT];
     __shared__ __align__(8) uint64_t mbar;
@@ -1094,7 +1098,7 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
             const double e2 = (dz ? 0.0 : box[1][box_pos<BX0>(1, j, l, q, j0, l0, q0, o1)]) + rsig[1][a * 8 + c];
             const double e3 = (dz ? 0.0 : box[2][box_pos<BX0>(2, j, l, q, j0, l0, q0, o2)]) + rsig[2][b * 8 + c];
             const double mu = ((e1 + e2) + e3) / 3.0;
-            mean[e] = mu;
+            mean[a * MA + b * MB + c] = mu;
             A.D[rbase[0][e >> 3] + (unsigned)(q - (q > j) - (q > l))] = mu;  // row (j,l), column q'
         }
     }
@@ -1108,13 +1112,13 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
             const int a = j0 + x, b = q0 + y, f = l0 + z;
             const unsigned base = rbase[1][e >> 3];
             if (base != NOIDX && f < n && f != a && f != b)
-                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[x * 64 + z * 8 + y];
+                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[x * MA + z * MB + y];
         }
         {   // view 2: row (l, q) = (l0 + x, q0 + y), free j = j0 + z; class (z, x, y)
             const int a = l0 + x, b = q0 + y, f = j0 + z;
             const unsigned base = rbase[2][e >> 3];
             if (base != NOIDX && f < n && f != a && f != b)
-                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[z * 64 + x * 8 + y];
+                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[z * MA + x * MB + y];
         }
     }
 }
