@@ -281,10 +281,11 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
 }
 
 // One column per lane (m <= 32): the same algorithm and the same floating-point
-// operations as warp_lap_solve<CPL>, with the column id equal to the lane id.  The
+// operations as warp_lap_solve<CPL>, with column c held by lane 31 - c (Mlane points at the
+// lane's column), so that "lowest column index" is the highest set lane bit (one FLO).  The
 // argmin takes the order key's high word first (the low word only on ties, a warp-uniform
 // branch), then prefers a free column (a lane mask updated once per augmentation), then
-// the lowest lane; the augmenting path is collected as one lane mask.
+// the lowest column; way[] and the augmenting path (one lane mask) are in lane ids.
 template <bool COUNT>
 __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int lane, int &poff, double &v,
                                                 double &ucol, int &steps)
@@ -294,8 +295,9 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
     poff = -1;
     int way = -1;
     const int rowb = m * 8;
-    const double minv0 = lane < m ? CUDART_INF : qnan();
-    uint32_t freemask = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    double minv0 = 31 - lane < m ? CUDART_INF : qnan();
+    asm("" : "+d"(minv0));  // keep it in registers (not rematerialised per row)
+    uint32_t freemask = m >= 32 ? 0xffffffffu : ~((1u << (32 - m)) - 1u);  // lanes 32-m .. 31
     for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
         double ucur = 0.0, ui0 = 0.0, minv = minv0, du = 0.0;
         int j0 = -1, i0off = i * rowb, j1;
@@ -318,7 +320,7 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
                 bal = __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
             }
             const uint32_t ft = bal & freemask;
-            j1 = __ffs(ft ? ft : bal) - 1;
+            j1 = 31 - __clz(ft ? ft : bal);  // highest lane = lowest column
             const double delta = __shfl_sync(FULL_MASK, minv, j1);
             const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
             const double nx_u = __shfl_sync(FULL_MASK, ucol, j1);
@@ -356,14 +358,14 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
 // evaluated when some raw residual is below -1e-9, from the original block `Mg` (global
 // memory, not yet overwritten — the residual is stored back after this returns).
 template <int CPL>
-__device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg, int m, int lane,
+__device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg, int m, int lane, int col0,
                                                     const int (&poff)[CPL], int (&p)[CPL], const double (&v)[CPL],
                                                     const double (&ucol)[CPL], double *urow, double *sel, bool &bad)
 {
     const int rowb = m * 8;
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
-        const int c = lane + 32 * t;
+        const int c = col0 + 32 * t;
         p[t] = c < m ? poff[t] / rowb : -1;
         if (c < m) {
             urow[p[t]] = ucol[t];
@@ -374,7 +376,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
     bool neg = false;  // some raw residual below -1e-9 (<= -tau candidates)
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
-        const int c = lane + 32 * t;
+        const int c = col0 + 32 * t;
         if (c < m) {
             double *Mc = M + c;
             const double vc = v[t];
@@ -400,7 +402,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
         double mx = 0.0, mn = 0.0;
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
-            const int c = lane + 32 * t;
+            const int c = col0 + 32 * t;
             if (c < m)
                 for (int r = 0; r < m; r++) {
                     const double g = Mg[r * m + c];
@@ -483,6 +485,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
     if (a.ctl != nullptr && a.ctl->stopped) return;
     extern __shared__ __align__(16) unsigned char smem[];
     const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int col0 = CPL == 1 ? 31 - lane : lane;  // this lane's (first) column
     const int m = a.m;
     const size_t bufb = lap_buf_bytes(m, CPL);
     unsigned char *wbase = smem + (size_t)warp * lap_warp_smem(m, CPL, NBUF);
@@ -545,14 +548,14 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         double v[CPL], ucol[CPL];
         int steps = 0;
         if constexpr (CPL == 1) {
-            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M + lane, m, lane, poff[0], v[0], ucol[0], steps);
-            else warp_lap_solve1<false>(M + lane, m, lane, poff[0], v[0], ucol[0], steps);
+            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M + col0, m, lane, poff[0], v[0], ucol[0], steps);
+            else warp_lap_solve1<false>(M + col0, m, lane, poff[0], v[0], ucol[0], steps);
         } else {
             if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M + lane, m, lane, poff, v, ucol, steps);
             else warp_lap_solve<CPL, false>(M + lane, m, lane, poff, v, ucol, steps);
         }
         bool bad;
-        const double S = warp_lap_epilogue<CPL>(M, a.src + b * a.ld, m, lane, poff, p, v, ucol, urow, sel, bad);
+        const double S = warp_lap_epilogue<CPL>(M, a.src + b * a.ld, m, lane, col0, poff, p, v, ucol, urow, sel, bad);
         anybad |= bad;
         if (lane == 0) {
             tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         if (a.lvl == LAP_BATCH) {
 #pragma unroll
             for (int t = 0; t < CPL; t++) {
-                const int c = lane + 32 * t;
+                const int c = col0 + 32 * t;
                 if (c < m) {
                     if (a.bo.assign) a.bo.assign[b * m + p[t]] = c;
                     if (a.bo.u) a.bo.u[b * m + p[t]] = ucol[t];
