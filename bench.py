@@ -105,13 +105,14 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic(kernel):
-    """dram read+write bytes per launch from the committed ncu --set full summary, if any."""
+def profiled_traffic(kernel, key="dram_bytes_per_launch"):
+    """Per-launch figure (dram read+write bytes, warp instructions) of the committed ncu
+    --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         d = json.load(open(p))
         if kernel in d:
-            return d[kernel].get("dram_bytes_per_launch")
+            return d[kernel].get(key)
     return None
 
 
@@ -385,6 +386,15 @@ def main():
                                        "transfer": "k_transfer"}[dom],
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": profiled_traffic(dom), "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
+    ins = profiled_traffic(dom, "inst_executed_per_launch")
+    if ins:  # what actually bounds the LAP kernel: warp-instruction issue
+        sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        mhz = clk.summary().get("sm_mhz") or 1965.0
+        slots = 4 * sms * mhz * 1e6 * per[dom]["avg_ms"] / 1e3
+        roof["issue"] = {"warp_inst_per_launch": ins, "issue_slots_per_launch": slots, "frac": ins / slots,
+                         "source": "instructions: committed ncu capture (profiles/traffic.json); slots: "
+                                   "4 schedulers x SMs x median SM clock x live CUDA-event duration",
+                         "note": "the level-2 LAP kernel is bound by warp-instruction issue, not by HBM"}
     iter_ms = (per["sigma"]["avg_ms"] + per["transfer"]["avg_ms"] + per["lap2"]["avg_ms"]
                + per["lap1"]["avg_ms"] * T / (T + 1) + per["lap0"]["avg_ms"])
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,

@@ -42,7 +42,8 @@ if __name__ == "__main__":
             continue
         s = summarise(rep, k)
         json.dump(s, open(f"profiles/{rnd}/ncu_{k}.json", "w"), indent=1)
-        traffic[k] = {"dram_bytes_per_launch": s["dram_bytes_per_launch"], "source": f"profiles/{rnd}/ncu_{k}.json",
+        traffic[k] = {"dram_bytes_per_launch": s["dram_bytes_per_launch"],
+                      "inst_executed_per_launch": s["inst_executed"], "source": f"profiles/{rnd}/ncu_{k}.json",
                       "capture": f"{tag} ncu --set full, N=30 nug seed 1"}
         print(k, json.dumps(s)[:600])
     json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
