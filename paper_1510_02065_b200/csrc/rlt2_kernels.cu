@@ -450,6 +450,7 @@ struct LapArgs {
     int ntile3;    // transfer CTAs per facility triple
     int64_t bdiv, bstr;  // level 1: B index of block b = (b / bdiv) * bstr + b % bdiv (batched RLT1)
     double *lbm;         // LAP_L0_MULTI: lbm[b] += S
+    int chunk;           // dynamic mode: blocks per work-queue grab (set by the launcher)
 };
 
 // First (canonical) facility of stored block b; `hint` only moves forward.
@@ -494,7 +495,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
     uint64_t *mbar = reinterpret_cast<uint64_t *>(wbase + NBUF * bufb + (((size_t)2 * m * 8 + 15) & ~size_t(15)));
 
     const bool dyn = a.sched != nullptr;
-    constexpr int CH = 4;  // blocks per work-queue grab (dynamic mode)
+    const int CH = a.chunk;  // blocks per work-queue grab (dynamic mode)
     const int64_t nw = (int64_t)gridDim.x * wpc;
     int64_t b, cend;
     if (dyn) {
@@ -1329,7 +1330,12 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     int64_t cap = (int64_t)num_sms * per_sm;
     if (a.sched) cap = (int64_t)num_sms * (per_sm < ctas_per_sm ? per_sm : ctas_per_sm);
     const int grid = (int)(want < cap ? want : cap);
-    k_lap<CPL, NBUF><<<grid, 32 * wpc, smem, st>>>(a);
+    // grabs of 4 blocks amortise the queue's atomics when every warp gets many LAPs; when the
+    // LAPs barely fill the resident warps (small B&B nodes) every warp should take one
+    LapArgs b = a;
+    const int64_t warps = (int64_t)grid * wpc;
+    b.chunk = a.count >= 8 * warps ? 4 : (a.count >= 3 * warps ? 2 : 1);
+    k_lap<CPL, NBUF><<<grid, 32 * wpc, smem, st>>>(b);
     return cudaGetLastError();
 }
 
