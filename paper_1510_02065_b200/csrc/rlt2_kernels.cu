@@ -871,7 +871,7 @@ constexpr unsigned NOIDX = 0xffffffffu;
 // its views 0 and 1 (members e1, e2) on owner(i) and its view 2 (member e3) on owner(k).
 enum { TK_LOCAL = 0, TK_AGG = 1, TK_HOLD = 2 };
 
-template <bool SHARDED>
+template <bool SHARDED, bool WIDE>  // WIDE: 64-bit per-view bases (>= 2^32 stored entries)
 __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
 {
     if (A.ctl->stopped) return;
@@ -902,6 +902,13 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
     const int tid = threadIdx.x;
     // which views live here
     const bool has01 = kind != TK_HOLD, has2 = kind != TK_AGG;
+    // 64-bit base block of each view (local numbering); 32-bit row offsets relative to it
+    const int n1 = n - 1;
+    const int64_t lo_i = SHARDED ? A.loc_off[i] : 0, lo_k = SHARDED ? A.loc_off[k] : 0;
+    const int64_t vb0 = WIDE ? g.off[i] + (int64_t)j0 * (n1 - i) * n1 + (int64_t)(k - i - 1) * n1 + lo_i : 0,
+                  vb1 = WIDE ? g.off[i] + (int64_t)j0 * (n1 - i) * n1 + (int64_t)(p - i - 1) * n1 + lo_i : 0,
+                  vb2 = WIDE ? g.off[k] + (int64_t)l0 * (n1 - k) * n1 + (int64_t)(p - k - 1) * n1 + lo_k : 0;
+    auto vbs = [&](int vw) { return vw == 0 ? vb0 : (vw == 1 ? vb1 : vb2); };
 
     // rows: view 0 = D{ij,kl} row p-2 (rows (j,l)); view 1 = D{ij,pq} row k-1 (rows (j,q));
     //       view 2 = D{kl,pq} row i   (rows (l,q)).  sigma is fetched now, used after the
@@ -921,7 +928,7 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
             else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; }
             else { bb = bid_of(g, k, r0, p, r1); row = i; }
             sg = A.sigma[bb];
-            base = (unsigned)((bb + (SHARDED ? A.loc_off[vw == 2 ? k : i] : 0)) * ld2 + row * m2);
+            base = (unsigned)((bb + (SHARDED ? A.loc_off[vw == 2 ? k : i] : 0) - vbs(vw)) * ld2 + row * m2);
         }
         rbase[vw][tid & 63] = base;
     }
@@ -944,7 +951,7 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
             unsigned ad = NOIDX;
             if (base != NOIDX && f < n && f != a && f != b) ad = base + (unsigned)(f - (f > a) - (f > b));
             addr[h][vw] = ad;
-            val[h][vw] = (ad != NOIDX && !A.d_zero) ? A.D[ad] : 0.0;
+            val[h][vw] = (ad != NOIDX && !A.d_zero) ? A.D[vbs(vw) * ld2 + ad] : 0.0;
         }
     }
     if (tid < 3 * TT * TT) rsig[tid >> 6][tid & 63] = sg;
@@ -987,7 +994,7 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
         const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
 #pragma unroll
         for (int vw = 0; vw < 3; vw++)
-            if (addr[h][vw] != NOIDX) A.D[addr[h][vw]] = sv[vw][tix(x, y, z)];
+            if (addr[h][vw] != NOIDX) A.D[vbs(vw) * ld2 + addr[h][vw]] = sv[vw][tix(x, y, z)];
     }
     if (A.publish) {  // overlapped mode: this tile of facility i is final (release)
         __threadfence();
@@ -1033,7 +1040,9 @@ __device__ __forceinline__ int box_pos(int vw, int j, int l, int q, int j0, int 
     }
 }
 
-template <int BX0>  // TT + 2 (m2 even: window starts are even) or TT + 4
+// WIDE: the stored D has >= 2^32 entries (n >= 47): row offsets relative to 64-bit per-view
+// base blocks; otherwise absolute 32-bit element indices (fewer instructions).
+template <int BX0, bool WIDE>  // BX0 = TT + 2 (m2 even: window starts are even) or TT + 4
 __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, const __grid_constant__ TmaMaps M)
 {
     constexpr int BOXE = TT * kBox1 * BX0;
@@ -1043,7 +1052,7 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
     // the permuted reads of the store phase are bank-conflict free)
     constexpr int MB = TT + 1, MA = TT * MB + 1;
     __shared__ double mean[TT * MA];
-    __shared__ unsigned rbase[3][TT * TT];
+    __shared__ unsigned rbase[3][TT * TT];  // element offset of each view row from the view's base
     __shared__ double rsig[3][TT * TT];
     __shared__ __align__(8) uint64_t mbar;
     const Geom &g = A.g;
@@ -1053,6 +1062,13 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
     const int i = tri & 0xff, k = (tri >> 8) & 0xff, p = tri >> 16;
     const int tile = blockIdx.x, tl = tile / ntile, tj = tl / ntile;
     const int q0 = (tile - tl * ntile) * TT, l0 = (tl - tj * ntile) * TT, j0 = tj * TT;
+    // WIDE: 64-bit base block of each view (first row location at the tile origin, second at
+    // 0); row offsets relative to it stay below 8 (n-1)^2 blocks, so 32 bits suffice for any n
+    const int n1 = n - 1;
+    const int64_t vb0 = WIDE ? g.off[i] + (int64_t)j0 * (n1 - i) * n1 + (int64_t)(k - i - 1) * n1 : 0;
+    const int64_t vb1 = WIDE ? g.off[i] + (int64_t)j0 * (n1 - i) * n1 + (int64_t)(p - i - 1) * n1 : 0;
+    const int64_t vb2 = WIDE ? g.off[k] + (int64_t)l0 * (n1 - k) * n1 + (int64_t)(p - k - 1) * n1 : 0;
+    double *const D0 = A.D + vb0 * ld2, *const D1 = A.D + vb1 * ld2, *const D2 = A.D + vb2 * ld2;
     const int tid = threadIdx.x;
     const bool dz = A.d_zero != 0;
     // dim0 window starts (entries) of the three views, before rounding down to even
@@ -1077,13 +1093,13 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
         unsigned base = NOIDX;
         double sg = 0.0;
         if (r0 < n && r1 < n && r0 != r1) {
-            int64_t bb;
+            int64_t bb, vb;
             int row;
-            if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; }
-            else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; }
-            else { bb = bid_of(g, k, r0, p, r1); row = i; }
+            if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; vb = vb0; }
+            else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; vb = vb1; }
+            else { bb = bid_of(g, k, r0, p, r1); row = i; vb = vb2; }
             sg = A.sigma[bb];
-            base = (unsigned)(bb * ld2 + row * m2);
+            base = (unsigned)((bb - vb) * ld2 + row * m2);
         }
         rbase[vw][tid & 63] = base;
         rsig[vw][tid & 63] = sg;
@@ -1103,7 +1119,7 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
             const double e3 = (dz ? 0.0 : box[2][box_pos<BX0>(2, j, l, q, j0, l0, q0, o2)]) + rsig[2][b * 8 + c];
             const double mu = ((e1 + e2) + e3) / 3.0;
             mean[a * MA + b * MB + c] = mu;
-            A.D[rbase[0][e >> 3] + (unsigned)(q - (q > j) - (q > l))] = mu;  // row (j,l), column q'
+            D0[rbase[0][e >> 3] + (unsigned)(q - (q > j) - (q > l))] = mu;  // row (j,l), column q'
         }
     }
     __syncthreads();
@@ -1116,13 +1132,13 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
             const int a = j0 + x, b = q0 + y, f = l0 + z;
             const unsigned base = rbase[1][e >> 3];
             if (base != NOIDX && f < n && f != a && f != b)
-                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[x * MA + z * MB + y];
+                D1[base + (unsigned)(f - (f > a) - (f > b))] = mean[x * MA + z * MB + y];
         }
         {   // view 2: row (l, q) = (l0 + x, q0 + y), free j = j0 + z; class (z, x, y)
             const int a = l0 + x, b = q0 + y, f = j0 + z;
             const unsigned base = rbase[2][e >> 3];
             if (base != NOIDX && f < n && f != a && f != b)
-                A.D[base + (unsigned)(f - (f > a) - (f > b))] = mean[z * MA + x * MB + y];
+                D2[base + (unsigned)(f - (f > a) - (f > b))] = mean[z * MA + x * MB + y];
         }
     }
 }
@@ -1267,21 +1283,30 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
     const int n = A.g.n;
     const int ntri = n * (n - 1) * (n - 2) / 6;
     dim3 grid(A.ntile * A.ntile * A.ntile, ntri);
-    if (tma_box0(n) == kBox0) k_transfer_tma<kBox0><<<grid, 256, 0, st>>>(A, M);
-    else k_transfer_tma<kBox0 - 2><<<grid, 256, 0, st>>>(A, M);
+    const bool wide = (int64_t)A.g.nblk * A.g.ld2 >= (int64_t(1) << 32);
+    if (tma_box0(n) == kBox0) {
+        if (wide) k_transfer_tma<kBox0, true><<<grid, 256, 0, st>>>(A, M);
+        else k_transfer_tma<kBox0, false><<<grid, 256, 0, st>>>(A, M);
+    } else {
+        if (wide) k_transfer_tma<kBox0 - 2, true><<<grid, 256, 0, st>>>(A, M);
+        else k_transfer_tma<kBox0 - 2, false><<<grid, 256, 0, st>>>(A, M);
+    }
     return cudaGetLastError();
 }
 
 cudaError_t launch_transfer(const TransferArgs &A, int ntiles_list, cudaStream_t st)
 {
     const int n = A.g.n;
+    const bool wide = (int64_t)A.g.nblk * A.g.ld2 >= (int64_t(1) << 32);  // global size: conservative
     if (A.tiles) {
         if (ntiles_list <= 0) return cudaSuccess;
-        k_transfer<true><<<ntiles_list, 256, 0, st>>>(A);
+        if (wide) k_transfer<true, true><<<ntiles_list, 256, 0, st>>>(A);
+        else k_transfer<true, false><<<ntiles_list, 256, 0, st>>>(A);
     } else {
         const int ntri = n * (n - 1) * (n - 2) / 6;
         dim3 grid(A.ntile * A.ntile * A.ntile, ntri);
-        k_transfer<false><<<grid, 256, 0, st>>>(A);
+        if (wide) k_transfer<false, true><<<grid, 256, 0, st>>>(A);
+        else k_transfer<false, false><<<grid, 256, 0, st>>>(A);
     }
     return cudaGetLastError();
 }
