@@ -480,12 +480,17 @@ __device__ __forceinline__ void wait_transfer(const LapArgs &a_, int a, int &rea
     fence_proxy_async_global();
 }
 
-template <int CPL, int NBUF>
+// WAIT: overlapped mode (QAP_FLAG_OVERLAP), blocks wait for the transfer of their facility.
+// Control flow is kept provably warp-uniform for ptxas (warp index and the stop flag read
+// through a shuffle; the transfer wait loop only in the WAIT instantiation): otherwise every
+// redux/shfl of the solver is guarded by a BRA.DIV pair (~15% of the Dijkstra step's issue).
+template <int CPL, int NBUF, bool WAIT>
 __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
 {
-    if (a.ctl != nullptr && a.ctl->stopped) return;
+    if (a.ctl != nullptr && __shfl_sync(FULL_MASK, a.ctl->stopped, 0)) return;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int wpc = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpc = blockDim.x >> 5, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0),
+              lane = threadIdx.x & 31;
     const int col0 = CPL == 1 ? 31 - lane : lane;  // this lane's (first) column
     const int m = a.m;
     const size_t bufb = lap_buf_bytes(m, CPL);
@@ -514,7 +519,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         fence_mbar_init();
-        if (dyn) wait_transfer(a, facility_of(a.g, b, hint_load), ready);
+        if (WAIT) wait_transfer(a, facility_of(a.g, b, hint_load), ready);
         mbar_expect_tx(&mbar[0], bytes);
         tma_load_1d(wbase, a.src + b * a.ld, bytes, &mbar[0]);
     }
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         }
         const int slot = NBUF == 2 ? (it & 1) : 0;
         if (NBUF == 2 && lane == 0 && nb < a.count) {
-            if (dyn) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
+            if (WAIT) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
             bulk_wait_read();  // the residual store out of the other buffer has read it
             mbar_expect_tx(&mbar[slot ^ 1], bytes);
             tma_load_1d(wbase + (slot ^ 1) * bufb, a.src + nb * a.ld, bytes, &mbar[slot ^ 1]);
@@ -561,7 +566,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         if (lane == 0) {
             tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global
             if (NBUF == 1 && nb < a.count) {          // buffer free once the store has read it
-                if (dyn) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
+                if (WAIT) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
                 bulk_wait_read();
                 mbar_expect_tx(&mbar[0], bytes);
                 tma_load_1d(wbase, a.src + nb * a.ld, bytes, &mbar[0]);
@@ -1321,7 +1326,7 @@ cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, do
     return cudaGetLastError();
 }
 
-template <int CPL, int NBUF>
+template <int CPL, int NBUF, bool WAIT>
 static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
 {
     const size_t smem = lap_warp_smem(a.m, CPL, NBUF) * wpc;
@@ -1339,7 +1344,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
             int mx = 0;
             if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
                 return e0;
-            if ((e0 = cudaFuncSetAttribute(k_lap<CPL, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
+            if ((e0 = cudaFuncSetAttribute(k_lap<CPL, NBUF, WAIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
                 cudaSuccess)
                 return e0;
             if (dev < 64) done_dev |= 1ull << dev;
@@ -1348,7 +1353,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     if (smem > 232448) return cudaErrorInvalidValue;
     cudaError_t e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF>, 32 * wpc, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF, WAIT>, 32 * wpc, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t want = (a.count + wpc - 1) / wpc;
@@ -1360,7 +1365,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     LapArgs b = a;
     const int64_t warps = (int64_t)grid * wpc;
     b.chunk = a.count >= 8 * warps ? 4 : (a.count >= 3 * warps ? 2 : 1);
-    k_lap<CPL, NBUF><<<grid, 32 * wpc, smem, st>>>(b);
+    k_lap<CPL, NBUF, WAIT><<<grid, 32 * wpc, smem, st>>>(b);
     return cudaGetLastError();
 }
 
@@ -1377,9 +1382,18 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
     if (cps <= 0) cps = 1;
     const size_t cap = (size_t)226 * 1024 / (a.sched ? cps : 1);
     while (wpc > 1 && lap_warp_smem(a.m, cpl, nbuf) * wpc > cap) wpc--;
+    if (a.sched && a.ntile3 > 0) {  // overlapped with the transfer: blocks wait for their facility
+        if (cpl == 1)
+            return nbuf == 2 ? launch_lap_on<1, 2, true>(a, num_sms, wpc, cps, st)
+                             : launch_lap_on<1, 1, true>(a, num_sms, wpc, cps, st);
+        return nbuf == 2 ? launch_lap_on<2, 2, true>(a, num_sms, wpc, cps, st)
+                         : launch_lap_on<2, 1, true>(a, num_sms, wpc, cps, st);
+    }
     if (cpl == 1)
-        return nbuf == 2 ? launch_lap_on<1, 2>(a, num_sms, wpc, cps, st) : launch_lap_on<1, 1>(a, num_sms, wpc, cps, st);
-    return nbuf == 2 ? launch_lap_on<2, 2>(a, num_sms, wpc, cps, st) : launch_lap_on<2, 1>(a, num_sms, wpc, cps, st);
+        return nbuf == 2 ? launch_lap_on<1, 2, false>(a, num_sms, wpc, cps, st)
+                         : launch_lap_on<1, 1, false>(a, num_sms, wpc, cps, st);
+    return nbuf == 2 ? launch_lap_on<2, 2, false>(a, num_sms, wpc, cps, st)
+                     : launch_lap_on<2, 1, false>(a, num_sms, wpc, cps, st);
 }
 
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B, Ctl *ctl,
