@@ -120,6 +120,7 @@ struct TransferArgs {
     const Ctl *ctl;
     Sched *sched;
     int ntile;            // ceil(n / TT)
+    unsigned ntile_mul;   // ceil(2^16 / ntile): y / ntile = (y * ntile_mul) >> 16 for y < 64 (set by the launcher)
     int publish;          // overlapped mode: publish per-facility progress
     // sharded iteration (nullptr tiles: every tile, single rank)
     const int *tiles;     // this rank's tiles (global tile id = triple * ntile^3 + tile)

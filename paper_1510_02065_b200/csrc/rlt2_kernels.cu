@@ -867,6 +867,20 @@ __global__ void k_sigma(const Geom g, const double *__restrict__ B, const double
 // and written back the same way — every stored entry is read once and written once.
 // ---------------------------------------------------------------------------------------
 
+// x / 3.0 correctly rounded (reading R11's division) without the IEEE division sequence:
+// q0 = RN(x y) with y = RN(1/3) = (1 - 2^-54)/3, r = x - 3 q0 exactly (one FMA), q1 = RN(q0 + r y)
+// (one FMA).  Writing d = x/3 - q0, the FMA's exact operand is q0 + r y = x/3 - d 2^-54, within
+// 2^-55 ulp of x/3; x/3 is never a rounding midpoint and lies at least ulp/6 away from one
+// (a 53-bit x would have to equal 3 M for a 54-bit odd M), so RN(x/3 - d 2^-54) = RN(x/3) for
+// every normal x and for 0.  Bit-identical to the oracle's (e1 + e2 + e3) / 3.0.
+__device__ __forceinline__ double div3(double x)
+{
+    const double y = 0x1.5555555555555p-2;  // RN(1/3)
+    const double q0 = __dmul_rn(x, y);
+    const double r = fma(-3.0, q0, x);
+    return fma(r, y, q0);
+}
+
 // Shared-memory index of element (x,y,z) of a tile view: rows padded to 9 doubles so
 // that the transposed reads of the mean phase are (nearly) bank-conflict free.
 __device__ __forceinline__ int tix(int x, int y, int z) { return x * (TT * (TT + 1)) + y * (TT + 1) + z; }
@@ -984,7 +998,7 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
             } else {
                 const double s12 = (SHARDED && kind == TK_HOLD) ? A.recvbuf[xo + e] : sv[0][e1] + sv[1][e2];
                 const double h3 = (SHARDED && kind == TK_AGG) ? A.recvbuf[xo + e] : sv[2][e3];
-                const double mu = (s12 + h3) / 3.0;
+                const double mu = div3(s12 + h3);
                 sv[0][e1] = mu;
                 sv[1][e2] = mu;
                 sv[2][e3] = mu;
@@ -1063,10 +1077,11 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
     const Geom &g = A.g;
     const int n = g.n, m2 = n - 2, ntile = A.ntile;
     const int64_t ld2 = g.ld2;
-    const int tri = A.triples[blockIdx.y];
+    const int tri = A.triples[blockIdx.z];
     const int i = tri & 0xff, k = (tri >> 8) & 0xff, p = tri >> 16;
-    const int tile = blockIdx.x, tl = tile / ntile, tj = tl / ntile;
-    const int q0 = (tile - tl * ntile) * TT, l0 = (tl - tj * ntile) * TT, j0 = tj * TT;
+    // grid (q tile, j tile * ntile + l tile, triple); y / ntile by a multiply (y < ntile^2 <= 64)
+    const int tj = (int)((blockIdx.y * A.ntile_mul) >> 16), tl = (int)blockIdx.y - tj * ntile;
+    const int q0 = (int)blockIdx.x * TT, l0 = tl * TT, j0 = tj * TT;
     // WIDE: 64-bit base block of each view (first row location at the tile origin, second at
     // 0); row offsets relative to it stay below 8 (n-1)^2 blocks, so 32 bits suffice for any n
     const int n1 = n - 1;
@@ -1098,13 +1113,18 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
         unsigned base = NOIDX;
         double sg = 0.0;
         if (r0 < n && r1 < n && r0 != r1) {
-            int64_t bb, vb;
-            int row;
-            if (vw == 0) { bb = bid_of(g, i, r0, k, r1); row = p - 2; vb = vb0; }
-            else if (vw == 1) { bb = bid_of(g, i, r0, p, r1); row = k - 1; vb = vb1; }
-            else { bb = bid_of(g, k, r0, p, r1); row = i; vb = vb2; }
-            sg = A.sigma[bb];
-            base = (unsigned)((bb - vb) * ld2 + row * m2);
+            // block D{f r0, h r1} (f < h): row `row`; 32-bit arithmetic unless WIDE
+            const int f = vw == 2 ? k : i, h = vw == 0 ? k : p, row = vw == 0 ? p - 2 : (vw == 1 ? k - 1 : i);
+            const int rel = r0 * (n1 - f) * n1 + (h - f - 1) * n1 + (r1 - (r1 > r0));  // block id - off[f]
+            if (WIDE) {
+                const int64_t bb = g.off[f] + rel;
+                sg = A.sigma[bb];
+                base = (unsigned)((bb - (vw == 0 ? vb0 : (vw == 1 ? vb1 : vb2))) * ld2 + row * m2);
+            } else {
+                const unsigned bb = (unsigned)g.off[f] + (unsigned)rel;
+                sg = A.sigma[bb];
+                base = bb * (unsigned)ld2 + (unsigned)(row * m2);
+            }
         }
         rbase[vw][tid & 63] = base;
         rsig[vw][tid & 63] = sg;
@@ -1122,7 +1142,7 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
             const double e1 = (dz ? 0.0 : box[0][box_pos<BX0>(0, j, l, q, j0, l0, q0, o0)]) + rsig[0][a * 8 + b];
             const double e2 = (dz ? 0.0 : box[1][box_pos<BX0>(1, j, l, q, j0, l0, q0, o1)]) + rsig[1][a * 8 + c];
             const double e3 = (dz ? 0.0 : box[2][box_pos<BX0>(2, j, l, q, j0, l0, q0, o2)]) + rsig[2][b * 8 + c];
-            const double mu = ((e1 + e2) + e3) / 3.0;
+            const double mu = div3((e1 + e2) + e3);
             mean[a * MA + b * MB + c] = mu;
             D0[rbase[0][e >> 3] + (unsigned)(q - (q > j) - (q > l))] = mu;  // row (j,l), column q'
         }
@@ -1287,14 +1307,17 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
 {
     const int n = A.g.n;
     const int ntri = n * (n - 1) * (n - 2) / 6;
-    dim3 grid(A.ntile * A.ntile * A.ntile, ntri);
+    if (A.ntile > 8 || ntri > 65535) return cudaErrorInvalidValue;  // n <= kMaxN = 64
+    TransferArgs B = A;
+    B.ntile_mul = (65536u + (unsigned)A.ntile - 1u) / (unsigned)A.ntile;  // exact y / ntile for y < 64
+    dim3 grid(A.ntile, A.ntile * A.ntile, ntri);
     const bool wide = (int64_t)A.g.nblk * A.g.ld2 >= (int64_t(1) << 32);
     if (tma_box0(n) == kBox0) {
-        if (wide) k_transfer_tma<kBox0, true><<<grid, 256, 0, st>>>(A, M);
-        else k_transfer_tma<kBox0, false><<<grid, 256, 0, st>>>(A, M);
+        if (wide) k_transfer_tma<kBox0, true><<<grid, 256, 0, st>>>(B, M);
+        else k_transfer_tma<kBox0, false><<<grid, 256, 0, st>>>(B, M);
     } else {
-        if (wide) k_transfer_tma<kBox0 - 2, true><<<grid, 256, 0, st>>>(A, M);
-        else k_transfer_tma<kBox0 - 2, false><<<grid, 256, 0, st>>>(A, M);
+        if (wide) k_transfer_tma<kBox0 - 2, true><<<grid, 256, 0, st>>>(B, M);
+        else k_transfer_tma<kBox0 - 2, false><<<grid, 256, 0, st>>>(B, M);
     }
     return cudaGetLastError();
 }
