@@ -286,6 +286,12 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
 // argmin takes the order key's high word first (the low word only on ties, a warp-uniform
 // branch), then prefers a free column (a lane mask updated once per augmentation), then
 // the lowest column; way[] and the augmenting path (one lane mask) are in lane ids.
+__device__ __noinline__ uint32_t tie_low_word(double minv, uint32_t sg, uint32_t hi, uint32_t mhi)
+{
+    const uint32_t lo = static_cast<uint32_t>(__double2loint(minv)) ^ sg;
+    const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
+    return __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
+}
 template <bool COUNT>
 __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int lane, int &poff, double &v,
                                                 double &ucol, int &steps)
@@ -314,11 +320,7 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
             const uint32_t hi = hb ^ (sg | 0x80000000u);
             const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
             uint32_t bal = __ballot_sync(FULL_MASK, hi == mhi);
-            if (bal & (bal - 1u)) {
-                const uint32_t lo = static_cast<uint32_t>(__double2loint(minv)) ^ sg;
-                const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
-                bal = __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
-            }
+            if (bal & (bal - 1u)) bal = tie_low_word(minv, sg, hi, mhi);
             const uint32_t ft = bal & freemask;
             j1 = 31 - __clz(ft ? ft : bal);  // highest lane = lowest column
             const double delta = __shfl_sync(FULL_MASK, minv, j1);
