@@ -453,6 +453,9 @@ struct LapArgs {
     int64_t bdiv, bstr;  // level 1: B index of block b = (b / bdiv) * bstr + b % bdiv (batched RLT1)
     double *lbm;         // LAP_L0_MULTI: lbm[b] += S
     int chunk;           // dynamic mode: blocks per work-queue grab (set by the launcher)
+    // level 2: x / d = umulhi(x, ceil(2^32 / d)) (exact for x d < 2^32) for d = n - 1 and
+    // d = (n - 1 - i)(n - 1), the block-id decode of the S credit (no integer division)
+    uint32_t mag_n1, mag_pj[kMaxN];
 };
 
 // First (canonical) facility of stored block b; `hint` only moves forward.
@@ -585,11 +588,11 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
                 const Geom &g = a.g;
                 facility_of(g, b, icur);
                 const int n = g.n, n1 = n - 1;
-                int rem = (int)(b - g.off[icur]);  // < n (n-1)^2: 32-bit divisions only
+                int rem = (int)(b - g.off[icur]);  // < n (n-1)^2
                 const int per_j = (n1 - icur) * n1;
-                const int j = rem / per_j;
+                const int j = (int)__umulhi((unsigned)rem, a.mag_pj[icur]);  // rem / per_j
                 rem -= j * per_j;
-                const int kk = rem / n1;
+                const int kk = (int)__umulhi((unsigned)rem, a.mag_n1);  // rem / n1
                 const int li = rem - kk * n1;
                 const int i = icur, k = i + 1 + kk, l = li + (li >= j);
                 // C was spread to D and zeroed: c <- 0 + S = S.
@@ -1437,6 +1440,11 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
     case LAP_L2:
         a.m = n - 2; a.count = g.nblk; a.ld = g.ld2; a.src = D; a.dst = D;
         wpc = lap_warps;
+        a.mag_n1 = (uint32_t)((0x100000000ull + (uint64_t)(n - 2)) / (uint64_t)(n - 1));
+        for (int i = 0; i + 1 < n; i++) {
+            const uint64_t d = (uint64_t)(n - 1 - i) * (uint64_t)(n - 1);
+            a.mag_pj[i] = (uint32_t)((0x100000000ull + d - 1) / d);
+        }
         a.sched = sched;
         {
             const int nt = (n + TT - 1) / TT;
