@@ -68,6 +68,10 @@ typedef struct {
                                      internal streams (experimental; default: one after the other) */
 #define QAP_FLAG_NO_GRAPH 4       /* do not replay the iteration loop from a cached CUDA graph     */
 #define QAP_FLAG_LDG_TRANSFER 8   /* transfer with per-element loads instead of tensor-map TMA    */
+#define QAP_FLAG_BLOCK_LAYOUT 16  /* keep the level-2 dual in the stored-block layout at every node
+                                     size (default: nodes with n >= 16 are bounded in the class
+                                     layout of DESIGN.md §6; results are bit-identical either way,
+                                     and qap_rlt2_dual_copy always exports the block layout)      */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */

@@ -89,6 +89,15 @@ struct qap_rlt2 {
     // tensor maps of D for k_transfer_tma, encoded for node size tma_n (0: none / failed)
     TmaMaps tma{};
     int tma_n = 0;
+    // class layout X of the level-2 dual: allocated for n_cap >= kXMin on
+    // single-rank handles; the block buffer dD is then allocated on first need (bytesD).
+    // dvalid: bit 0 = dD holds the current D, bit 1 = dX does (both while D is lazily zero).
+    double *dX = nullptr;
+    size_t bytesD = 0;
+    int dvalid = 3;
+    CUtensorMap xmap{};   // 4-D [np][n][n][3 ntri], 8x8x8x1 boxes (k_transfer_x)
+    CUtensorMap xrow{};   // 2-D [3 ntri n n][np], {np, 1} boxes (level-2 LAP gather4/scatter4)
+    int xmap_n = 0;
 };
 
 static std::string g_create_error;
@@ -158,6 +167,7 @@ static void free_all(qap_rlt2 *h)
     cudaFree(h->dB);
     cudaFree(h->dC);
     cudaFree(h->dD);
+    cudaFree(h->dX);
     cudaFree(h->dSigma);
     cudaFree(h->dTrace);
     cudaFree(h->dCtl);
@@ -205,6 +215,8 @@ static qap_status check_instance(qap_rlt2 *h, int N, const int64_t *F, const int
 }
 
 extern "C" {
+static qap_status d_layout(qap_rlt2 *h, int want);
+static qap_status ensure_dD(qap_rlt2 *h);
 
 static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
                               qap_rlt2 **out, bool loopback, int n_cap = 0);
@@ -281,7 +293,12 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         delete h;
         return s;
     }
-    const size_t need = bytesD + bytesC + bytesB + bytesS + (64u << 20);
+    // class layout unless the flags pin the block-layout kernels
+    const bool xl = world == 1 && !loopback && h->n_cap >= kXMin &&
+                    !(h->flags & (QAP_FLAG_BLOCK_LAYOUT | QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER));
+    const size_t bytesX = xl ? x_doubles(h->n_cap) * 8 : 0;
+    h->bytesD = bytesD;
+    const size_t need = (xl ? bytesX : bytesD) + bytesC + bytesB + bytesS + (64u << 20);
     if (need > freeb) {
         delete h;
         char msg[160];
@@ -299,7 +316,11 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
     ALLOC(h->dDist, (size_t)N * N * 8);
     ALLOC(h->dB, bytesB);
     ALLOC(h->dC, bytesC);
-    ALLOC(h->dD, bytesD);
+    if (xl) {
+        ALLOC(h->dX, bytesX);
+    } else {
+        ALLOC(h->dD, bytesD);
+    }
     ALLOC(h->dSigma, bytesS);
     ALLOC(h->dTrace, (size_t)h->trace_cap * 8);
     ALLOC(h->dCtl, sizeof(Ctl));
@@ -432,6 +453,7 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
     if (e != cudaSuccess) return cuda_fail(h, e, "k_init");
     h->next_phase = PH_FRESH;
     h->d_zero = 1;
+    h->dvalid = 3;
     h->b_zero = 0;
     h->c_zero = 0;
     return QAP_OK;
@@ -468,6 +490,10 @@ qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, i
     }
     cudaError_t e = cudaSetDevice(child->device);
     if (e != cudaSuccess) return cuda_fail(child, e, "device");
+    qap_rlt2 *par = const_cast<qap_rlt2 *>(parent);
+    qap_status ls = d_layout(par, 1);  // the fold reads the parent's stored blocks
+    if (ls != QAP_OK) return fail(child, ls, "parent layout: " + par->err);
+    if ((ls = ensure_dD(child)) != QAP_OK) return ls;
     // order: parent's pending work -> fold (child stream) -> later parent work
     if ((e = cudaEventRecord(parent->evJoin, parent->stream)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(child->stream, parent->evJoin, 0)) != cudaSuccess)
@@ -497,6 +523,7 @@ qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, i
         return cuda_fail(child, e, "fold ordering");
     child->next_phase = PH_FRESH;
     child->d_zero = parent->d_zero;
+    child->dvalid = parent->d_zero ? 3 : 1;
     child->b_zero = 0;
     child->c_zero = 0;
     return QAP_OK;
@@ -606,6 +633,79 @@ static bool tma_maps(qap_rlt2 *h)
     return ok;
 }
 
+// ---- layouts of the level-2 dual ----------------------------------------
+// 4-D tensor map of the class layout X for node size n: [np][n][n][3 ntri], 8x8x8x1 boxes
+static bool x_map(qap_rlt2 *h)
+{
+    const Geom &g = h->geom;
+    if (!h->dX) return false;
+    if (h->xmap_n == g.n) return true;
+    if (h->xmap_n == -g.n) return false;
+    auto enc = tma_encoder();
+    bool ok = enc != nullptr && g.n >= TT;
+    if (ok) {
+        const cuuint64_t np = (cuuint64_t)g.np, n = (cuuint64_t)g.n;
+        cuuint64_t dims[4] = {np, n, n, 3 * (cuuint64_t)g.ntri};
+        cuuint64_t strides[3] = {np * 8, n * np * 8, n * n * np * 8};
+        cuuint32_t box[4] = {(cuuint32_t)TT, (cuuint32_t)TT, (cuuint32_t)TT, 1u};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        ok = enc(&h->xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dX, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        cuuint64_t dims2[2] = {np, 3 * (cuuint64_t)g.ntri * n * n};
+        cuuint64_t strides2[1] = {np * 8};
+        // box width = the LAP's cost-buffer row stride (>= n + 2, multiple of 4): the columns
+        // beyond np are zero-filled on load and clipped on store
+        cuuint32_t box2[2] = {(cuuint32_t)((g.n + 5) & ~3), 1u};
+        ok = ok && enc(&h->xrow, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->dX, dims2, strides2, box2, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    h->xmap_n = ok ? g.n : -g.n;
+    return ok;
+}
+// the current node is bounded in the class layout
+static bool use_x(qap_rlt2 *h)
+{
+    return h->dX && h->world == 1 && !h->loopback && h->geom.n >= kXMin &&
+           !(h->flags & (QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER | QAP_FLAG_BLOCK_LAYOUT)) && x_map(h);
+}
+static qap_status ensure_dD(qap_rlt2 *h)
+{
+    if (h->dD) return QAP_OK;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&h->dD), h->bytesD);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(h, QAP_E_CAPACITY, "block-layout buffer: cudaMalloc failed");
+    }
+    return e != cudaSuccess ? cuda_fail(h, e, "cudaMalloc") : QAP_OK;
+}
+// make layout `want` (1: stored blocks dD, 2: class layout dX) hold the current D,
+// converting on the handle's stream (never inside a graph capture)
+static qap_status d_layout(qap_rlt2 *h, int want)
+{
+    if (want == 1) {
+        qap_status s = ensure_dD(h);
+        if (s != QAP_OK) return s;
+    }
+    if (h->d_zero) {  // lazily zero: both layouts hold it
+        h->dvalid = 3;
+        return QAP_OK;
+    }
+    if (h->dvalid & want) return QAP_OK;
+    if (!(h->dvalid & 3) || (want == 2 && !h->dX)) return fail(h, QAP_E_STATE, "no layout holds D");
+    cudaError_t e = launch_xconv(h->geom, h->dD, h->dX, want == 2, h->num_sms, h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "layout conversion");
+    h->dvalid |= want;
+    return QAP_OK;
+}
+// before enqueueing iterations: the layout the kernels of this node use holds D
+static qap_status prepare_layout(qap_rlt2 *h)
+{
+    if (h->world > 1 || h->loopback) return QAP_OK;
+    return d_layout(h, use_x(h) ? 2 : 1);
+}
+
 static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused)
 {
     cudaError_t e = cudaSuccess;
@@ -652,13 +752,17 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
                 if ((e = cudaEventRecord(h->evS, sT)) != cudaSuccess) return e;
                 if ((e = cudaStreamWaitEvent(sL, h->evS, 0)) != cudaSuccess) return e;
             }
-            const TransferArgs A = transfer_args(h, ov ? 1 : 0);
-            const bool tma = !ov && !(h->flags & QAP_FLAG_LDG_TRANSFER) && tma_maps(h);
+            TransferArgs A = transfer_args(h, ov ? 1 : 0);
+            const bool xl = !ov && use_x(h);
+            const bool tma = !xl && !ov && !(h->flags & QAP_FLAG_LDG_TRANSFER) && tma_maps(h);
+            if (xl) A.D = h->dX;
             e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {
-                return tma ? launch_transfer_tma(A, h->tma, s) : launch_transfer(A, 0, s);
+                return xl ? launch_transfer_x(A, h->xmap, s)
+                          : (tma ? launch_transfer_tma(A, h->tma, s) : launch_transfer(A, 0, s));
             });
             if (e) return e;
             h->d_zero = 0;
+            h->dvalid = xl ? 2 : 1;
             h->b_zero = h->c_zero = 1;
             if (!fused) break;
         }
@@ -666,11 +770,13 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
         // (LAP warps spin on the transfer's progress counters; co-residency => progress)
         int cfg = h->lap_warps;
         if (ov) cfg = (cfg & ~0xf0ff) | ((cfg & 0xff) && (cfg & 0xff) < 16 ? (cfg & 0xff) : 16);
+        const bool xl = !ov && use_x(h);
         e = launch(h, QAP_K_LAP2, sL, [&](cudaStream_t s) {
             return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, cfg, h->dSched,
-                                    ov ? 1 : 0, s);
+                                    ov ? 1 : 0, s, xl ? h->dX : nullptr, &h->xrow);
         });
         if (e) return e;
+        h->dvalid = xl ? 2 : 1;
         if (ov) {  // LAP2 finishes after the transfer (it waited for every facility)
             if ((e = cudaEventRecord(h->evL, sL)) != cudaSuccess) return e;
             if ((e = cudaStreamWaitEvent(st, h->evL, 0)) != cudaSuccess) return e;
@@ -713,6 +819,10 @@ qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase)
     const int expect = h->next_phase == PH_FRESH ? QAP_PHASE_ITER0 : h->next_phase;
     if (phase != expect) return fail(h, QAP_E_STATE, "phases must run in Algorithm-1 order");
     h->call_launches = 0;
+    if (phase == QAP_PHASE_TRANSFER || phase == QAP_PHASE_CONC_D) {
+        qap_status s = prepare_layout(h);
+        if (s != QAP_OK) return s;
+    }
     cudaError_t e = launch_ctl_begin(h->dCtl, 0.0, INFINITY, h->trace_cap, h->stream);
     if (e == cudaSuccess) e = run_phase(h, phase, h->stream, false);
     if (e != cudaSuccess) return cuda_fail(h, e, "step");
@@ -739,6 +849,10 @@ qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double
     if (h->loopback) return fail(h, QAP_E_STATE, "in-process group member: use qap_rlt2_group_bound");
     if (h->geom.n < 3) return fail(h, QAP_E_STATE, "the handle holds no node");
     h->call_launches = 0;
+    if (max_iters > 0) {
+        qap_status s = prepare_layout(h);
+        if (s != QAP_OK) return s;
+    }
     cudaError_t e = launch_ctl_begin(h->dCtl, K, UB, h->trace_cap, h->stream);
     h->call_launches++;
     if (e != cudaSuccess) return cuda_fail(h, e, "ctl");
@@ -777,6 +891,7 @@ qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double
         h->call_launches += 4 * max_iters;  // kernels in the graph: sigma, transfer, lap2, lap1, lap0
         h->call_launches += max_iters;
         h->d_zero = 0;
+        h->dvalid = use_x(h) ? 2 : 1;  // the replayed kernels wrote D in this layout
         h->b_zero = h->c_zero = 0;
     } else {
         for (int t = 0; t < max_iters; t++) {
@@ -915,6 +1030,11 @@ qap_status qap_rlt2_dual_copy(const qap_rlt2 *hc, double *B, double *C, double *
         if (h->c_zero) memset(C, 0, w * n * n);
         else if ((e = cudaMemcpy2D(C, w, h->dC, g.ldc * 8, w, n * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
             return cuda_fail(h, e, "copy C");
+    }
+    if (D && h->world == 1 && !h->loopback && !h->d_zero && !(h->dvalid & 1)) {
+        qap_status s = d_layout(h, 1);  // export layout: stored blocks
+        if (s != QAP_OK) return s;
+        if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cuda_fail(h, e, "sync");
     }
     if (D) {
         const size_t w = (size_t)(n - 2) * (n - 2) * 8;
@@ -1358,6 +1478,10 @@ qap_status Bnb::copy_state(qap_rlt2 *dst, const qap_rlt2 *src)
     const Geom &g = src->geom;
     if (g.n > dst->n_cap) return fail(dst, QAP_E_CAPACITY, "state copy: node larger than the target");
     cudaError_t e;
+    qap_rlt2 *s0 = const_cast<qap_rlt2 *>(src);
+    qap_status ls = d_layout(s0, 1);  // copies go through the stored-block layout
+    if (ls != QAP_OK) return fail(dst, ls, "state copy: " + s0->err);
+    if ((ls = ensure_dD(dst)) != QAP_OK) return ls;
     if ((e = cudaEventRecord(src->evJoin, src->stream)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(dst->stream, src->evJoin, 0)) != cudaSuccess)
         return cuda_fail(dst, e, "state copy ordering");
@@ -1378,6 +1502,7 @@ qap_status Bnb::copy_state(qap_rlt2 *dst, const qap_rlt2 *src)
     dst->geom = src->geom;
     dst->next_phase = src->next_phase;
     dst->d_zero = src->d_zero;
+    dst->dvalid = src->d_zero ? 3 : 1;
     dst->b_zero = src->b_zero;
     dst->c_zero = src->c_zero;
     return QAP_OK;

@@ -121,6 +121,46 @@ __device__ __forceinline__ int64_t bid_of(const Geom &g, int i, int j, int k, in
     return g.off[i] + (int64_t)j * (n1 - i) * n1 + (int64_t)(k - i - 1) * n1 + (l - (l > j));
 }
 
+// Class layout X (see k_transfer_x): row runs of stored blocks.
+__device__ __forceinline__ int tri_index(int n, int a, int b, int c)
+{
+    const int A = n - a, K = A - 1, bb = b - a - 1, Kb = K - bb;
+    return (n * (n - 1) * (n - 2) - A * (A - 1) * (A - 2)) / 6 + (K * (K - 1) - Kb * (Kb - 1)) / 2 + (c - b - 1);
+}
+// row p (p != i, k) of stored block D{ij,kl} (i < k): index of its run in units of np doubles
+__device__ __forceinline__ unsigned x_row(const Geom &g, int i, int j, int k, int l, int p)
+{
+    int r, t;
+    if (p > k) { r = 0; t = tri_index(g.n, i, k, p); }
+    else if (p > i) { r = 1; t = tri_index(g.n, i, p, k); }
+    else { r = 2; t = tri_index(g.n, p, i, k); }
+    return ((unsigned)(r * g.ntri + t) * (unsigned)g.n + (unsigned)j) * (unsigned)g.n + (unsigned)l;
+}
+// location of column s of a block whose pairs hold locations j and l (reading R7)
+__device__ __forceinline__ int x_col(int s, int j, int l)
+{
+    const int lo = j < l ? j : l, hi = j < l ? l : j;
+    const int q = s + (s >= lo);
+    return q + (q >= hi);
+}
+// facility of row r of a block whose pairs hold facilities i < k
+__device__ __forceinline__ int x_rowfac(int r, int i, int k)
+{
+    const int p = r + (r >= i);
+    return p + (p >= k);
+}
+
+__device__ __forceinline__ void cp_async8(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------------------
 // The warp LAP solver (reading R4/R5/R6).  Lane `lane` owns columns
 // c = lane + 32 t (t < CPL).  Per column, in registers: v (dual), ucol = u of the row
@@ -293,14 +333,14 @@ __device__ __noinline__ uint32_t tie_low_word(double minv, uint32_t sg, uint32_t
     return __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
 }
 template <bool COUNT>
-__device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int lane, int &poff, double &v,
+__device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int ldm, int lane, int &poff, double &v,
                                                 double &ucol, int &steps)
 {
     v = 0.0;
     ucol = 0.0;
     poff = -1;
     int way = -1;
-    const int rowb = m * 8;
+    const int rowb = ldm * 8;  // bytes per cost row
     double minv0 = 31 - lane < m ? CUDART_INF : qnan();
     asm("" : "+d"(minv0));  // keep it in registers (not rematerialised per row)
     uint32_t freemask = m >= 32 ? 0xffffffffu : ~((1u << (32 - m)) - 1u);  // lanes 32-m .. 31
@@ -357,21 +397,25 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
 // (reading R9).  Returns S (all lanes) and sets `bad` if some residual fell below -tau.
 // p[t] receives the matched row of each owned column.  One pass: the clamp to +0 is
 // applied directly; since tau >= 1e-9, the exact tau test (which needs max|M|) is only
-// evaluated when some raw residual is below -1e-9, from the original block `Mg` (global
-// memory, not yet overwritten — the residual is stored back after this returns).
-template <int CPL>
-__device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg, int m, int lane, int col0,
-                                                    const int (&poff)[CPL], int (&p)[CPL], const double (&v)[CPL],
-                                                    const double (&ucol)[CPL], double *urow, double *sel, bool &bad)
+// evaluated when some raw residual is below -1e-9, from the original block: Mg(r, t, c)
+// returns entry (r, c) from global memory, not yet overwritten — the residual is stored
+// back after this returns (called by all lanes; c >= m: value unused).
+// Rows of the cost buffer are ldm doubles apart; column c of owned slot t sits at offset
+// cofs[t] within a row (the block layout: ldm = m, cofs = c).
+template <int CPL, class GVal>
+__device__ __forceinline__ double warp_lap_epilogue(double *M, GVal Mg, int m, int ldm, const int (&cofs)[CPL],
+                                                    int lane, int col0, const int (&poff)[CPL], int (&p)[CPL],
+                                                    const double (&v)[CPL], const double (&ucol)[CPL], double *urow,
+                                                    double *sel, int ust, bool &bad)
 {
-    const int rowb = m * 8;
+    const int rowb = ldm * 8;
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         const int c = col0 + 32 * t;
         p[t] = c < m ? poff[t] / rowb : -1;
         if (c < m) {
-            urow[p[t]] = ucol[t];
-            sel[p[t]] = M[p[t] * m + c];
+            urow[p[t] * ust] = ucol[t];
+            sel[p[t] * ust] = M[p[t] * ldm + cofs[t]];
         }
     }
     __syncwarp();
@@ -380,23 +424,23 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
     for (int t = 0; t < CPL; t++) {
         const int c = col0 + 32 * t;
         if (c < m) {
-            double *Mc = M + c;
+            double *Mc = M + cofs[t];
             const double vc = v[t];
 #pragma unroll 4
             for (int r = 0; r < m; r++) {
-                const double x = (Mc[r * m] - urow[r]) - vc;
+                const double x = (Mc[r * ldm] - urow[r * ust]) - vc;
                 neg |= x < -1e-9;
                 // x <= 0 (incl. -0) -> +0, else x (== x > 0.0 ? x : 0.0 for every non-NaN x):
                 // clear both words when the sign bit is set
                 const int hi = __double2hiint(x), lo = __double2loint(x), keep = ~(hi >> 31);
-                Mc[r * m] = __hiloint2double(hi & keep, lo & keep);
+                Mc[r * ldm] = __hiloint2double(hi & keep, lo & keep);
             }
-            Mc[p[t] * m] = 0.0;  // assigned cell -> +0
+            Mc[p[t] * ldm] = 0.0;  // assigned cell -> +0
         }
     }
     double S = 0.0;
     if (lane == 0)
-        for (int r = 0; r < m; r++) S = S + sel[r];  // sequential row order (reading R9)
+        for (int r = 0; r < m; r++) S = S + sel[r * ust];  // sequential row order (reading R9)
     S = __shfl_sync(FULL_MASK, S, 0);
     bad = false;
     if (__any_sync(FULL_MASK, neg)) {  // rare: exact test tau = 1e-9 max(1, max|M|)
@@ -405,13 +449,14 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             const int c = col0 + 32 * t;
-            if (c < m)
-                for (int r = 0; r < m; r++) {
-                    const double g = Mg[r * m + c];
-                    const double x = (g - urow[r]) - v[t];
+            for (int r = 0; r < m; r++) {  // warp-uniform loop: Mg may shuffle
+                const double g = Mg(r, t, c);
+                if (c < m) {
+                    const double x = (g - urow[r * ust]) - v[t];
                     mn = x < mn ? x : mn;
                     mx = fmax(mx, fabs(g));
                 }
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -428,13 +473,27 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, const double *Mg,
 // Shared memory per warp: NBUF cost buffers (TMA destinations; m*m doubles plus 32*CPL
 // doubles of padding so that every lane may load its column of any row unconditionally),
 // urow[m], sel[m], 2 mbarriers — packed tightly so that 32 warps fit one SM at m = 28.
-__host__ __device__ inline size_t lap_buf_bytes(int m, int cpl)
+// ldrow > 0: the class layout with one column per lane (rows of ldrow doubles moved whole by
+// per-lane TMA bulk copies; columns are per-lane offsets, lanes without one read a junk slot)
+__host__ __device__ inline size_t lap_buf_bytes(int m, int cpl, int ldrow = 0)
 {
+    if (ldrow > 0) return ((size_t)m * ldrow * 8 + 15) & ~size_t(15);
     return (((size_t)m * m + 32 * cpl) * 8 + 15) & ~size_t(15);
 }
-__host__ __device__ inline size_t lap_warp_smem(int m, int cpl, int nbuf)
+__host__ __device__ inline size_t lap_warp_smem(int m, int cpl, int nbuf, int ldrow = 0)
 {
+    // ldrow > 0 (class layout, one column per lane): rows in groups of 4 moved by TMA gather4 /
+    // scatter4 (128-byte aligned groups: ldrow % 4 == 0), u and the selected entry of row r kept
+    // in the row's spare columns n and n + 1 (ldrow >= n + 2), one mbarrier per warp at the end
+    if (ldrow > 0) return (size_t)((m + 3) & ~3) * ldrow * 8 + 16;
     return nbuf * lap_buf_bytes(m, cpl) + (((size_t)2 * m * 8 + 15) & ~size_t(15)) + 16;
+}
+
+// First (canonical) facility of stored block b; `hint` only moves forward.
+__device__ __forceinline__ int facility_of(const Geom &g, int64_t b, int &hint)
+{
+    while (hint + 1 < g.n && b >= g.off[hint + 1]) hint++;
+    return hint;
 }
 
 struct LapArgs {
@@ -456,14 +515,158 @@ struct LapArgs {
     // level 2: x / d = umulhi(x, ceil(2^32 / d)) (exact for x d < 2^32) for d = n - 1 and
     // d = (n - 1 - i)(n - 1), the block-id decode of the S credit (no integer division)
     uint32_t mag_n1, mag_pj[kMaxN];
+    double *X;  // level 2 in the class layout (k_lap<..., XL = true>): blocks are row runs of X
+    const CUtensorMap *xrow;  // host: 2-D map [3 ntri n n][np] of X with {np, 1} boxes (gather4)
 };
-
-// First (canonical) facility of stored block b; `hint` only moves forward.
-__device__ __forceinline__ int facility_of(const Geom &g, int64_t b, int &hint)
+// TMA tile::gather4 / tile::scatter4 (sm_100a): four row runs of X <-> four consecutive
+// rows of the cost buffer in one instruction (2-D map, box {np, 1}; coordinates {0, rows})
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, unsigned r0, unsigned r1, unsigned r2,
+                                            unsigned r3, uint64_t *mbar)
 {
-    while (hint + 1 < g.n && b >= g.off[hint + 1]) hint++;
-    return hint;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(mbar))
+        : "memory");
 }
+// all row groups of one block: lane 0 issues one gather4 (load) or scatter4 (store) per 4
+// rows; row r's run index is held by lane r (x_rows), rows >= m by junk row 0
+template <bool LOAD>
+__device__ __forceinline__ void x_rows4(const CUtensorMap *tm, double *M, int ldm, int m4, unsigned xr, int lane,
+                                        uint64_t *mbar)
+{
+    const uint64_t tma = reinterpret_cast<uint64_t>(tm);
+    uint32_t sa = smem_u32(M);
+    const uint32_t gstep = (uint32_t)(4 * ldm * 8);
+    const uint32_t mb = smem_u32(mbar);
+#pragma unroll 1
+    for (int r = 0; r < m4; r += 4) {
+        const unsigned r0 = __shfl_sync(FULL_MASK, xr, r), r1 = __shfl_sync(FULL_MASK, xr, r + 1),
+                       r2 = __shfl_sync(FULL_MASK, xr, r + 2), r3 = __shfl_sync(FULL_MASK, xr, r + 3);
+        if (lane == 0) {
+            if (LOAD)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], "
+                    "[%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(sa),
+                    "l"(tma), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(mb)
+                    : "memory");
+            else
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], "
+                    "[%6];" ::"l"(tma),
+                    "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(sa)
+                    : "memory");
+        }
+        sa += gstep;
+    }
+}
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap *tm, unsigned r0, unsigned r1, unsigned r2, unsigned r3,
+                                             const void *src)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+            reinterpret_cast<uint64_t>(tm)),
+        "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(src))
+        : "memory");
+}
+
+// Level 2: pairs (i,j), (k,l) of stored block b (i = canonical first facility; `icur` is a
+// hint that only moves forward), packed i | j << 8 | k << 16 | l << 24.
+__device__ __forceinline__ unsigned decode_l2(const LapArgs &a, int64_t b, int &icur)
+{
+    const Geom &g = a.g;
+    facility_of(g, b, icur);
+    const int n = g.n, n1 = n - 1;
+    int rem = (int)(b - g.off[icur]);  // < n (n-1)^2
+    const int per_j = (n1 - icur) * n1;
+    const int j = (int)__umulhi((unsigned)rem, a.mag_pj[icur]);  // rem / per_j
+    rem -= j * per_j;
+    const int kk = (int)__umulhi((unsigned)rem, a.mag_n1);  // rem / n1
+    const int li = rem - kk * n1;
+    const int k = icur + 1 + kk, l = li + (li >= j);
+    return (unsigned)icur | ((unsigned)j << 8) | ((unsigned)k << 16) | ((unsigned)l << 24);
+}
+
+// Class layout: run index (units of np doubles) of the rows lane + 32 u of the block.
+template <int CPL>
+__device__ __forceinline__ void x_rows(const Geom &g, unsigned ijkl, int m, int lane, unsigned (&xr)[CPL])
+{
+    const int i = ijkl & 0xff, j = (ijkl >> 8) & 0xff, k = (ijkl >> 16) & 0xff, l = ijkl >> 24;
+#pragma unroll
+    for (int u = 0; u < CPL; u++) {
+        const int r = lane + 32 * u;
+        xr[u] = r < m ? x_row(g, i, j, k, l, x_rowfac(r, i, k)) : 0u;
+    }
+}
+// Per owned column: its slot in a row run (a lane without a column, c >= m, uses the slot of
+// location j, which belongs to no class), and its cell of row 0 in the warp's cost buffer
+// with the row stride (c >= m: a padding cell, stride 0) — branch-free row loops.
+template <int CPL>
+struct XCols {
+    const double *g[CPL];  // X + slot
+    double *s[CPL];        // cost-buffer cell of row 0
+    int ss[CPL];           // cost-buffer row stride (doubles)
+};
+template <int CPL>
+__device__ __forceinline__ void x_cols(const double *X, double *M, unsigned ijkl, int m, int col0, XCols<CPL> &xc)
+{
+    const int j = (ijkl >> 8) & 0xff, l = ijkl >> 24;
+#pragma unroll
+    for (int t = 0; t < CPL; t++) {
+        const int c = col0 + 32 * t;
+        const bool own = c < m;
+        xc.g[t] = X + (own ? x_col(c, j, l) : j);
+        xc.s[t] = own ? M + c : M + m * m + (c - m);
+        xc.ss[t] = own ? m : 0;
+    }
+}
+template <int CPL>
+__device__ __forceinline__ unsigned x_pick(const unsigned (&xr)[CPL], int r)
+{
+    unsigned v = xr[0];
+#pragma unroll
+    for (int u = 1; u < CPL; u++)
+        if ((r >> 5) == u) v = xr[u];
+    return __shfl_sync(FULL_MASK, v, r & 31);
+}
+// asynchronous row-run loads of one block into the warp's cost buffer (cp.async, 8 B/lane)
+template <int CPL>
+__device__ __forceinline__ void x_load(int np, int m, const unsigned (&xr)[CPL], const XCols<CPL> &xc)
+{
+    uint32_t sa[CPL];
+#pragma unroll
+    for (int t = 0; t < CPL; t++) sa[t] = smem_u32(xc.s[t]);
+    const uint32_t np8 = (uint32_t)np * 8u;  // u32 x u32 -> u64: one IMAD.WIDE.U32 per row
+    for (int r = 0; r < m; r++) {
+        const uint64_t off = (uint64_t)x_pick<CPL>(xr, r) * np8;
+#pragma unroll
+        for (int t = 0; t < CPL; t++) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa[t]),
+                         "l"(reinterpret_cast<const char *>(xc.g[t]) + off)
+                         : "memory");
+            sa[t] += (uint32_t)xc.ss[t] * 8u;
+        }
+    }
+    cp_async_commit();
+}
+// residual rows of the cost buffer back to their runs
+template <int CPL>
+__device__ __forceinline__ void x_store(int np, int m, const unsigned (&xr)[CPL], const XCols<CPL> &xc)
+{
+    const double *sp[CPL];
+#pragma unroll
+    for (int t = 0; t < CPL; t++) sp[t] = xc.s[t];
+    const uint32_t np8 = (uint32_t)np * 8u;  // u32 x u32 -> u64: one IMAD.WIDE.U32 per row
+    for (int r = 0; r < m; r++) {
+        const uint64_t off = (uint64_t)x_pick<CPL>(xr, r) * np8;
+#pragma unroll
+        for (int t = 0; t < CPL; t++) {
+            *reinterpret_cast<double *>(const_cast<char *>(reinterpret_cast<const char *>(xc.g[t])) + off) = *sp[t];
+            sp[t] += xc.ss[t];
+        }
+    }
+}
+
 
 // Lane 0 only: block until the transfer of every facility <= a has finished (acquire),
 // then order those generic-proxy writes before our async-proxy (TMA) reads.
@@ -489,20 +692,26 @@ __device__ __forceinline__ void wait_transfer(const LapArgs &a_, int a, int &rea
 // Control flow is kept provably warp-uniform for ptxas (warp index and the stop flag read
 // through a shuffle; the transfer wait loop only in the WAIT instantiation): otherwise every
 // redux/shfl of the solver is guarded by a BRA.DIV pair (~15% of the Dijkstra step's issue).
-template <int CPL, int NBUF, bool WAIT>
-__global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
+template <int CPL, int NBUF, bool WAIT, bool XL>
+__global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_constant__ CUtensorMap xrow)
 {
     if (a.ctl != nullptr && __shfl_sync(FULL_MASK, a.ctl->stopped, 0)) return;
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int wpc = blockDim.x >> 5, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0),
               lane = threadIdx.x & 31;
     const int col0 = CPL == 1 ? 31 - lane : lane;  // this lane's (first) column
     const int m = a.m;
-    const size_t bufb = lap_buf_bytes(m, CPL);
-    unsigned char *wbase = smem + (size_t)warp * lap_warp_smem(m, CPL, NBUF);
+    // XB: class layout, one column per lane: whole row runs by per-lane TMA bulk copies
+    constexpr bool XB = XL && CPL == 1;
+    const int ldm = XB ? ((a.g.n + 5) & ~3) : m;  // cost-buffer row stride (doubles); XB: >= n + 2, % 4 == 0
+    const int m4 = (m + 3) & ~3;                   // XB: rows moved in groups of 4 (gather4 / scatter4)
+    const size_t bufb = XB ? (size_t)m4 * ldm * 8 : lap_buf_bytes(m, CPL);
+    unsigned char *wbase = smem + (size_t)warp * (XB ? bufb : lap_warp_smem(m, CPL, NBUF));
     double *urow = reinterpret_cast<double *>(wbase + NBUF * bufb);
     double *sel = urow + m;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(wbase + NBUF * bufb + (((size_t)2 * m * 8 + 15) & ~size_t(15)));
+    uint64_t *mbar = XB ? reinterpret_cast<uint64_t *>(smem + (size_t)wpc * bufb + (size_t)warp * 16)
+                        : reinterpret_cast<uint64_t *>(wbase + NBUF * bufb + (((size_t)2 * m * 8 + 15) & ~size_t(15)));
+    double *const xurow = reinterpret_cast<double *>(wbase) + a.g.n, *const xsel = xurow + 1;  // XB: spare columns
 
     const bool dyn = a.sched != nullptr;
     const int CH = a.chunk;  // blocks per work-queue grab (dynamic mode)
@@ -520,7 +729,29 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
     if (b >= a.count) return;
     const uint32_t bytes = (uint32_t)(((int64_t)m * m + 1) & ~int64_t(1)) * 8u;
     int hint_load = 0, ready = -1;
-    if (lane == 0) {
+    int icur = 0;  // canonical first facility of block b (L2), advanced monotonically
+    unsigned ijkl = 0;  // XL: pairs of block b
+    unsigned xr[CPL];   // XL: row runs of block b
+    int cofs[CPL];      // offset of each owned column within a cost-buffer row
+#pragma unroll
+    for (int t = 0; t < CPL; t++) cofs[t] = col0 + 32 * t;
+    if (XB) {
+        ijkl = decode_l2(a, b, icur);
+        x_rows<CPL>(a.g, ijkl, m, lane, xr);
+        if (lane == 0) {
+            mbar_init(&mbar[0], 1);
+            fence_mbar_init();
+            mbar_expect_tx(&mbar[0], (uint32_t)(m4 * ldm * 8));
+        }
+        // rows >= m: junk row 0 (locations j = l = 0)
+        x_rows4<true>(&xrow, reinterpret_cast<double *>(wbase), ldm, m4, xr[0], lane, &mbar[0]);
+    } else if (XL) {
+        ijkl = decode_l2(a, b, icur);
+        x_rows<CPL>(a.g, ijkl, m, lane, xr);
+        XCols<CPL> xc;
+        x_cols<CPL>(a.X, reinterpret_cast<double *>(wbase), ijkl, m, col0, xc);
+        x_load<CPL>(a.g.np, m, xr, xc);
+    } else if (lane == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         fence_mbar_init();
@@ -530,7 +761,6 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
     }
     __syncwarp();
 
-    int icur = 0;  // canonical first facility of block b (L2), advanced monotonically
     bool anybad = false;
     for (int it = 0; b < a.count; it++) {
         int64_t nb;  // next block of this warp
@@ -552,23 +782,84 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
             mbar_expect_tx(&mbar[slot ^ 1], bytes);
             tma_load_1d(wbase + (slot ^ 1) * bufb, a.src + nb * a.ld, bytes, &mbar[slot ^ 1]);
         }
-        mbar_wait(&mbar[slot], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
+        if (XL && !XB) {
+            cp_async_wait();
+            __syncwarp();
+        } else {
+            mbar_wait(&mbar[slot], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
+        }
         double *M = reinterpret_cast<double *>(wbase + slot * bufb);
 
         int poff[CPL], p[CPL];
         double v[CPL], ucol[CPL];
         int steps = 0;
+        if (XB) {  // column c -> its location's slot (lanes without a column: slot of location j)
+            const int j = (ijkl >> 8) & 0xff, l = ijkl >> 24;
+            cofs[0] = col0 < m ? x_col(col0, j, l) : j;
+        }
         if constexpr (CPL == 1) {
-            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M + col0, m, lane, poff[0], v[0], ucol[0], steps);
-            else warp_lap_solve1<false>(M + col0, m, lane, poff[0], v[0], ucol[0], steps);
+            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M + cofs[0], m, ldm, lane, poff[0], v[0], ucol[0], steps);
+            else warp_lap_solve1<false>(M + cofs[0], m, ldm, lane, poff[0], v[0], ucol[0], steps);
         } else {
             if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M + lane, m, lane, poff, v, ucol, steps);
             else warp_lap_solve<CPL, false>(M + lane, m, lane, poff, v, ucol, steps);
         }
         bool bad;
-        const double S = warp_lap_epilogue<CPL>(M, a.src + b * a.ld, m, lane, col0, poff, p, v, ucol, urow, sel, bad);
+        double S;
+        unsigned nijkl = 0;
+        int inext = icur;
+        if (XB) {
+            const double *X = a.X;
+            S = warp_lap_epilogue<CPL>(
+                M,
+                [&](int r, int t, int c) {
+                    const double *src = X + (size_t)x_pick<CPL>(xr, r) * (size_t)a.g.np + cofs[t];
+                    return c < m ? *src : 0.0;
+                },
+                m, ldm, cofs, lane, col0, poff, p, v, ucol, xurow, xsel, ldm, bad);
+            // residual rows back to their runs (scatter4; rows >= m: junk row 0), then the
+            // next block's rows into the buffer once the stores have read it
+            x_rows4<false>(&xrow, M, ldm, m4, xr[0], lane, &mbar[0]);
+            if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            if (nb < a.count) {
+                inext = icur;
+                nijkl = decode_l2(a, nb, inext);
+                x_rows<CPL>(a.g, nijkl, m, lane, xr);
+                if (lane == 0) {
+                    bulk_wait_read();
+                    mbar_expect_tx(&mbar[0], (uint32_t)(m4 * ldm * 8));
+                }
+                x_rows4<true>(&xrow, M, ldm, m4, xr[0], lane, &mbar[0]);
+            }
+        } else if (XL) {
+            XCols<CPL> xc;
+            x_cols<CPL>(a.X, M, ijkl, m, col0, xc);
+            const int np = a.g.np;
+            S = warp_lap_epilogue<CPL>(
+                M,
+                [&](int r, int t, int c) {
+                    const double *src = xc.g[t] + (size_t)x_pick<CPL>(xr, r) * (size_t)np;
+                    return c < m ? *src : 0.0;
+                },
+                m, m, cofs, lane, col0, poff, p, v, ucol, urow, sel, 1, bad);
+            // residual rows back to their runs, then the next block's rows into the buffer
+            x_store<CPL>(np, m, xr, xc);
+            __syncwarp();
+            if (nb < a.count) {
+                inext = icur;
+                nijkl = decode_l2(a, nb, inext);
+                x_rows<CPL>(a.g, nijkl, m, lane, xr);
+                x_cols<CPL>(a.X, M, nijkl, m, col0, xc);
+                x_load<CPL>(np, m, xr, xc);
+            }
+        } else {
+            const double *Mg = a.src + b * a.ld;
+            S = warp_lap_epilogue<CPL>(
+                M, [&](int r, int t, int c) { return c < m ? Mg[r * m + c] : 0.0; }, m, m, cofs, lane, col0, poff, p,
+                v, ucol, urow, sel, 1, bad);
+        }
         anybad |= bad;
-        if (lane == 0) {
+        if (!XL && lane == 0) {
             tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global
             if (NBUF == 1 && nb < a.count) {          // buffer free once the store has read it
                 if (WAIT) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
@@ -586,15 +877,9 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
                     break;
                 }
                 const Geom &g = a.g;
-                facility_of(g, b, icur);
                 const int n = g.n, n1 = n - 1;
-                int rem = (int)(b - g.off[icur]);  // < n (n-1)^2
-                const int per_j = (n1 - icur) * n1;
-                const int j = (int)__umulhi((unsigned)rem, a.mag_pj[icur]);  // rem / per_j
-                rem -= j * per_j;
-                const int kk = (int)__umulhi((unsigned)rem, a.mag_n1);  // rem / n1
-                const int li = rem - kk * n1;
-                const int i = icur, k = i + 1 + kk, l = li + (li >= j);
+                const unsigned q = XL ? ijkl : decode_l2(a, b, icur);
+                const int i = q & 0xff, j = (q >> 8) & 0xff, k = (q >> 16) & 0xff, l = q >> 24;
                 // C was spread to D and zeroed: c <- 0 + S = S.
                 a.C[(int64_t)(i * n + j) * g.ldc + (k - 1) * n1 + (l - (l > j))] = S;
                 a.C[(int64_t)(k * n + l) * g.ldc + i * n1 + (j - (j > l))] = S;
@@ -655,6 +940,10 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
             }
         }
         __syncwarp();
+        if (XL) {
+            ijkl = nijkl;
+            icur = inext;
+        }
         b = nb;
     }
     if (lane == 0) bulk_wait_all();
@@ -1174,6 +1463,124 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
 }
 
 // ---------------------------------------------------------------------------------------
+// Class layout X.  The stored value of class member e of class
+// {(a,x),(b,y),(c,z)}, a < b < c (reading R11/R12), lives in section r of X,
+// where r is the position of the member's ROW facility in the sorted triple:
+//   r = 0: e1, block D{ax,by}, row c  ->  X[0][t][x][y][z]
+//   r = 1: e2, block D{ax,cz}, row b  ->  X[1][t][x][z][y]
+//   r = 2: e3, block D{by,cz}, row a  ->  X[2][t][y][z][x]
+// t = lexicographic index of (a,b,c).  In every section the index is
+// [t][block's first location][block's second location][row facility's location], so row p
+// of block D{ij,kl} is the contiguous run X[r][t][j][l][0..n) (columns q != j, l used):
+// the level-2 LAP reads and writes whole rows, and the transfer moves whole 8x8x8 boxes of
+// each section by tensor-map TMA (no skip-indexed windows, no overlap between tiles).
+// Slots with repeated locations belong to no class and are never read.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void tma_store_4d(const void *tmap, int c0, int c1, int c2, int c3, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+                 : "memory");
+}
+
+// k_transfer_x — spreading C->D fused with the transfer between the 3 members of every class
+// (reading R10/R11), in the class layout: one CTA per facility triple
+// t = (a,b,c) x 8x8x8 tile of locations (x,y,z).  The three sections' boxes are loaded by
+// TMA, every thread forms the mean of 2 classes with the oracle's operation order
+//   mu = ((e1 + sigma1) + (e2 + sigma2)) + (e3 + sigma3)) / 3,
+// writes it over the three member slots in shared memory, and the boxes are stored back by
+// TMA (out-of-range box parts are zero-filled on load and clipped on store).
+constexpr int kXT = 128;  // k_transfer_x threads per CTA (16 CTAs per SM: more tiles in flight)
+__global__ void __launch_bounds__(kXT, 16) k_transfer_x(const TransferArgs A, const __grid_constant__ CUtensorMap xm)
+{
+    if (A.ctl->stopped) return;
+    __shared__ __align__(128) double box[3][TT * TT * TT];
+    __shared__ double rsig[3][TT * TT];
+    __shared__ __align__(8) uint64_t mbar;
+    const Geom &g = A.g;
+    const int n = g.n, n1 = n - 1, ntile = A.ntile;
+    const int t = (int)blockIdx.z, tri = A.triples[t];
+    const int fa = tri & 0xff, fb = (tri >> 8) & 0xff, fc = tri >> 16;
+    const int tx = (int)((blockIdx.y * A.ntile_mul) >> 16), ty = (int)blockIdx.y - tx * ntile;
+    const int x0 = tx * TT, y0 = ty * TT, z0 = (int)blockIdx.x * TT;
+    const int tid = threadIdx.x;
+    const bool dz = A.d_zero != 0;
+    if (tid == 0 && !dz) {
+        mbar_init(&mbar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&mbar, 3u * TT * TT * TT * 8u);
+        tma_load_4d(box[0], &xm, z0, y0, x0, t, &mbar);              // [x][y][z]
+        tma_load_4d(box[1], &xm, y0, z0, x0, g.ntri + t, &mbar);     // [x][z][y]
+        tma_load_4d(box[2], &xm, x0, z0, y0, 2 * g.ntri + t, &mbar); // [y][z][x]
+    }
+    // sigma of each member's block (k_sigma): member 1 by (x,y), 2 by (x,z), 3 by (y,z)
+    for (int e = tid; e < 3 * TT * TT; e += kXT) {
+        const int vw = e >> 6, u = x0 * (vw < 2) + y0 * (vw == 2) + ((e >> 3) & 7),
+                  w = (vw == 0 ? y0 : z0) + (e & 7);
+        const int f = vw == 2 ? fb : fa, h = vw == 0 ? fb : fc;
+        double sg = 0.0;
+        if (u < n && w < n && u != w)
+            sg = A.sigma[(unsigned)g.off[f] + (unsigned)(u * (n1 - f) * n1 + (h - f - 1) * n1 + (w - (w > u)))];
+        rsig[vw][e & 63] = sg;
+    }
+    __syncthreads();
+    if (!dz) mbar_wait(&mbar, 0);
+#pragma unroll
+    for (int hh = 0; hh < TT * TT * TT / kXT; hh++) {
+        const int e = tid + kXT * hh;
+        const int u = e >> 6, v = (e >> 3) & 7, w = e & 7;
+        const int x = x0 + u, y = y0 + v, z = z0 + w;
+        if (x < n && y < n && z < n && x != y && x != z && y != z) {
+            const int p0 = (u * TT + v) * TT + w, p1 = (u * TT + w) * TT + v, p2 = (v * TT + w) * TT + u;
+            const double e1 = (dz ? 0.0 : box[0][p0]) + rsig[0][u * TT + v];
+            const double e2 = (dz ? 0.0 : box[1][p1]) + rsig[1][u * TT + w];
+            const double e3 = (dz ? 0.0 : box[2][p2]) + rsig[2][v * TT + w];
+            const double mu = div3((e1 + e2) + e3);
+            box[0][p0] = mu;
+            box[1][p1] = mu;
+            box[2][p2] = mu;
+        }
+    }
+    fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA stores
+    __syncthreads();
+    if (tid == 0) {
+        tma_store_4d(&xm, z0, y0, x0, t, box[0]);
+        tma_store_4d(&xm, y0, z0, x0, g.ntri + t, box[1]);
+        tma_store_4d(&xm, x0, z0, y0, 2 * g.ntri + t, box[2]);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        bulk_wait_read();  // shared memory stays valid until the stores have read it
+    }
+}
+
+// stored blocks <-> class layout (export, warm folds, A/B with the block path): one warp per
+// stored block, lanes over columns, rows streamed; valid entries only.
+__global__ void __launch_bounds__(256) k_xconv(const Geom g, double *__restrict__ D, double *__restrict__ X, int to_x)
+{
+    const int n = g.n, n1 = n - 1, m = n - 2, lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int hint = 0;
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < g.nblk; b += nw) {
+        while (hint + 1 < n && b >= g.off[hint + 1]) hint++;
+        while (hint > 0 && b < g.off[hint]) hint--;
+        const int i = hint;
+        int rem = (int)(b - g.off[i]);
+        const int per_j = (n1 - i) * n1, j = rem / per_j;
+        rem -= j * per_j;
+        const int k = i + 1 + rem / n1, li = rem % n1, l = li + (li >= j);
+        double *blk = D + b * g.ld2;
+        for (int r = 0; r < m; r++) {
+            const size_t row = (size_t)x_row(g, i, j, k, l, x_rowfac(r, i, k)) * (size_t)g.np;
+            for (int c = lane; c < m; c += 32) {
+                double *xs = X + row + x_col(c, j, l);
+                if (to_x) *xs = blk[r * m + c];
+                else blk[r * m + c] = *xs;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // Strong branching: RLT1 bounds of the n^2 candidate children of a node at once.
 // Child c = a * n + b fixes free facility I[a] at free location J[b] in addition to the
 // node's pairs; its reduced costs are built as in k_init (O0/O1).
@@ -1327,6 +1734,26 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
     return cudaGetLastError();
 }
 
+cudaError_t launch_transfer_x(const TransferArgs &A, const CUtensorMap &xmap, cudaStream_t st)
+{
+    const int n = A.g.n;
+    if (A.ntile > 8 || A.g.ntri > 65535) return cudaErrorInvalidValue;  // n <= kMaxN = 64
+    TransferArgs B = A;
+    B.ntile_mul = (65536u + (unsigned)A.ntile - 1u) / (unsigned)A.ntile;
+    dim3 grid(A.ntile, A.ntile * A.ntile, A.g.ntri);
+    (void)n;
+    k_transfer_x<<<grid, kXT, 0, st>>>(B, xmap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xconv(const Geom &g, double *D, double *X, int to_x, int num_sms, cudaStream_t st)
+{
+    int64_t blocks = (g.nblk + 7) / 8;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    k_xconv<<<(int)blocks, 256, 0, st>>>(g, D, X, to_x);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_transfer(const TransferArgs &A, int ntiles_list, cudaStream_t st)
 {
     const int n = A.g.n;
@@ -1354,10 +1781,10 @@ cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, do
     return cudaGetLastError();
 }
 
-template <int CPL, int NBUF, bool WAIT>
+template <int CPL, int NBUF, bool WAIT, bool XL = false>
 static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
 {
-    const size_t smem = lap_warp_smem(a.m, CPL, NBUF) * wpc;
+    const size_t smem = lap_warp_smem(a.m, CPL, NBUF, (XL && CPL == 1) ? ((a.g.n + 5) & ~3) : 0) * wpc;
     // The dynamic-smem limit is a process-wide attribute of the kernel: raise it once per
     // device to the opt-in maximum (setting it per launch to the exact size would race
     // between threads launching different sizes, e.g. concurrent B&B workers).
@@ -1372,7 +1799,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
             int mx = 0;
             if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
                 return e0;
-            if ((e0 = cudaFuncSetAttribute(k_lap<CPL, NBUF, WAIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
+            if ((e0 = cudaFuncSetAttribute(k_lap<CPL, NBUF, WAIT, XL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
                 cudaSuccess)
                 return e0;
             if (dev < 64) done_dev |= 1ull << dev;
@@ -1381,7 +1808,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     if (smem > 232448) return cudaErrorInvalidValue;
     cudaError_t e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF, WAIT>, 32 * wpc, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF, WAIT, XL>, 32 * wpc, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t want = (a.count + wpc - 1) / wpc;
@@ -1393,7 +1820,12 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     LapArgs b = a;
     const int64_t warps = (int64_t)grid * wpc;
     b.chunk = a.count >= 8 * warps ? 4 : (a.count >= 3 * warps ? 2 : 1);
-    k_lap<CPL, NBUF, WAIT><<<grid, 32 * wpc, smem, st>>>(b);
+    CUtensorMap xm{};
+    if (XL && CPL == 1) {
+        if (!a.xrow) return cudaErrorInvalidValue;
+        xm = *a.xrow;
+    }
+    k_lap<CPL, NBUF, WAIT, XL><<<grid, 32 * wpc, smem, st>>>(b, xm);
     return cudaGetLastError();
 }
 
@@ -1409,7 +1841,13 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
     int cps = (lap_cfg >> 12) & 0xf;
     if (cps <= 0) cps = 1;
     const size_t cap = (size_t)226 * 1024 / (a.sched ? cps : 1);
-    while (wpc > 1 && lap_warp_smem(a.m, cpl, nbuf) * wpc > cap) wpc--;
+    const int ldrow = (a.X && cpl == 1) ? ((a.g.n + 5) & ~3) : 0;
+    while (wpc > 1 && lap_warp_smem(a.m, cpl, nbuf, ldrow) * wpc > cap) wpc--;
+    if (a.X) {  // class layout (no overlap mode, single buffer)
+        if (a.sched && a.ntile3 > 0) return cudaErrorInvalidValue;
+        return cpl == 1 ? launch_lap_on<1, 1, false, true>(a, num_sms, wpc, cps, st)
+                        : launch_lap_on<2, 1, false, true>(a, num_sms, wpc, cps, st);
+    }
     if (a.sched && a.ntile3 > 0) {  // overlapped with the transfer: blocks wait for their facility
         if (cpl == 1)
             return nbuf == 2 ? launch_lap_on<1, 2, true>(a, num_sms, wpc, cps, st)
@@ -1425,7 +1863,8 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
 }
 
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B, Ctl *ctl,
-                             double *trace, int num_sms, int lap_warps, Sched *sched, int wait, cudaStream_t st)
+                             double *trace, int num_sms, int lap_warps, Sched *sched, int wait, cudaStream_t st,
+                             double *X, const CUtensorMap *xrow)
 {
     LapArgs a{};
     a.lvl = lvl;
@@ -1439,6 +1878,8 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
     switch (lvl) {
     case LAP_L2:
         a.m = n - 2; a.count = g.nblk; a.ld = g.ld2; a.src = D; a.dst = D;
+        a.X = X;
+        a.xrow = xrow;
         wpc = lap_warps;
         a.mag_n1 = (uint32_t)((0x100000000ull + (uint64_t)(n - 2)) / (uint64_t)(n - 1));
         for (int i = 0; i + 1 < n; i++) {
