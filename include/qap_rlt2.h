@@ -72,6 +72,10 @@ typedef struct {
                                      size (default: nodes with n >= 16 are bounded in the class
                                      layout of DESIGN.md §6; results are bit-identical either way,
                                      and qap_rlt2_dual_copy always exports the block layout)      */
+#define QAP_FLAG_FUSED 32         /* class layout, one column per lane (16 <= n <= 34): run each
+                                     iteration's transfer and level-2 LAPs as ONE persistent
+                                     kernel (warps take transfer tiles or LAPs whose facility is
+                                     transferred; bit-identical results)                         */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */

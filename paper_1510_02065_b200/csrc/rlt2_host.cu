@@ -97,6 +97,7 @@ struct qap_rlt2 {
     int dvalid = 3;
     CUtensorMap xmap{};   // 4-D [np][n][n][3 ntri], 8x8x8x1 boxes (k_transfer_x)
     CUtensorMap xrow{};   // 2-D [3 ntri n n][np], {np, 1} boxes (level-2 LAP gather4/scatter4)
+    CUtensorMap xa{}, xb{};  // 4-D as xmap with {8,8,4,1} / {4,8,8,1} boxes (k_fused_x tiles)
     int xmap_n = 0;
 };
 
@@ -660,6 +661,13 @@ static bool x_map(qap_rlt2 *h)
         ok = ok && enc(&h->xrow, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->dX, dims2, strides2, box2, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        cuuint32_t boxa[4] = {8u, 8u, 4u, 1u}, boxb[4] = {4u, 8u, 8u, 1u};
+        ok = ok && enc(&h->xa, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dX, dims, strides, boxa, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        ok = ok && enc(&h->xb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dX, dims, strides, boxb, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
     h->xmap_n = ok ? g.n : -g.n;
     return ok;
@@ -754,6 +762,20 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
             }
             TransferArgs A = transfer_args(h, ov ? 1 : 0);
             const bool xl = !ov && use_x(h);
+            if (xl && fused && (h->flags & QAP_FLAG_FUSED) && g.n - 2 <= 32) {
+                // transfer + level-2 LAPs in one persistent kernel (k_fused_x)
+                A.D = h->dX;
+                e = launch(h, QAP_K_LAP2, sT, [&](cudaStream_t s) {
+                    return launch_fused_x(g, A, h->dX, h->dC, h->dCtl, h->dSched, h->num_sms, h->xa, h->xb,
+                                          h->xrow, s);
+                });
+                if (e) return e;
+                h->d_zero = 0;
+                h->dvalid = 2;
+                h->b_zero = 1;
+                h->c_zero = 0;
+                break;
+            }
             const bool tma = !xl && !ov && !(h->flags & QAP_FLAG_LDG_TRANSFER) && tma_maps(h);
             if (xl) A.D = h->dX;
             e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {

@@ -31,6 +31,7 @@ struct Ctl {
 struct Sched {
     unsigned done[kMaxN];
     unsigned long long head;
+    unsigned long long thead;  // fused iteration (k_fused_x): transfer-tile queue
 };
 
 // Geometry of the reduced problem at the current node.
@@ -156,6 +157,13 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
 cudaError_t launch_transfer_x(const TransferArgs &A, const CUtensorMap &xmap, cudaStream_t st);
 // stored blocks <-> class layout X (to_x = 1: D -> X; 0: X -> D); valid entries only
 cudaError_t launch_xconv(const Geom &g, double *D, double *X, int to_x, int num_sms, cudaStream_t st);
+// One iteration's transfer and level-2 concentration in one persistent kernel over the class
+// layout (QAP_FLAG_FUSED): warps take 4x8x8 transfer tiles or level-2 LAPs
+// whose facility's transfer has completed.  xa / xb: 4-D maps of X with {8,8,4,1} / {4,8,8,1}
+// boxes; xrow: the 2-D row map of the level-2 LAP (gather4 / scatter4).
+cudaError_t launch_fused_x(const Geom &g, const TransferArgs &A, double *X, double *C, Ctl *ctl, Sched *sched,
+                           int num_sms, const CUtensorMap &xa, const CUtensorMap &xb, const CUtensorMap &xrow,
+                           cudaStream_t st);
 int tma_box0(int n);  // dim0 box extent for node size n (TT + 2 when n - 2 is even, else TT + 4)
 struct Offsets {
     int64_t off[kMaxN];

@@ -20,6 +20,7 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "rlt2_internal.h"
@@ -1135,7 +1136,10 @@ __global__ void k_sigma(const Geom g, const double *__restrict__ B, const double
     if (ctl->stopped) return;
     if (blockIdx.x == 0 && threadIdx.x < kMaxN) {
         sched->done[threadIdx.x] = 0;
-        if (threadIdx.x == 0) sched->head = 0;
+        if (threadIdx.x == 0) {
+            sched->head = 0;
+            sched->thead = 0;
+        }
     }
     const int n = g.n, n1 = n - 1;
     const int64_t n4 = (int64_t)n * n * n * n;
@@ -1731,6 +1735,288 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
         if (wide) k_transfer_tma<kBox0 - 2, true><<<grid, 256, 0, st>>>(B, M);
         else k_transfer_tma<kBox0 - 2, false><<<grid, 256, 0, st>>>(B, M);
     }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// k_fused_x — the transfer and the level-2 concentration of
+// one iteration in ONE persistent kernel over the class layout, so that the HBM-bound
+// transfer runs on the same SMs as the issue-bound LAPs instead of before them.  Every warp
+// is a worker with one 7 KB shared-memory buffer and takes either
+//   * a transfer tile: facility triple t x 4x8x8 locations — three TMA boxes, 8 class means
+//     per lane (the operation order of k_transfer_x), three TMA box stores, then the tile
+//     is published in done[smallest facility] (release), or
+//   * a level-2 LAP of a stored block D{ij,kl} (as k_lap<1,1,0,1>), once every triple with
+//     smallest facility <= min(i, n-3) is published: those are exactly the triples with a
+//     member in the block, and no later tile touches it (so the LAP may overwrite it).
+// Queues are in facility order.  One warp in four prefers transfer tiles; the others take
+// LAPs whenever the next one is ready and transfer tiles otherwise, so the transfer runs at
+// full width at the start of the iteration and whenever the LAPs catch up with it.  Transfer
+// tiles never wait: the kernel cannot deadlock.  The results are bit-identical to
+// k_transfer_x followed by k_lap (the same operations on the same values).
+// ---------------------------------------------------------------------------------------
+struct FusedArgs {
+    LapArgs L;
+    TransferArgs T;
+    int ntx, nyz;          // tiles: ceil(n / 4) x-tiles, ceil(n / 8) y- and z-tiles
+    int tpt;               // tiles per facility triple
+    long long ntiles;      // all transfer tiles
+    int wbytes;            // shared memory per warp buffer
+    int tmask;             // warps with (warp & tmask) == 0 prefer transfer tiles
+};
+constexpr int kFusedTileX = 4;
+__device__ __forceinline__ void fused_transfer_tile(const FusedArgs &F, long long job, double *buf, uint64_t *mbar,
+                                                    uint32_t &phase, int lane, const CUtensorMap *xa,
+                                                    const CUtensorMap *xb)
+{
+    const TransferArgs &A = F.T;
+    const Geom &g = A.g;
+    const int n = g.n, n1 = n - 1;
+    const int t = (int)(job / F.tpt);
+    int rem = (int)(job - (long long)t * F.tpt);
+    const int nyz2 = F.nyz * F.nyz;
+    const int tx = rem / nyz2;
+    rem -= tx * nyz2;
+    const int ty = rem / F.nyz, tz = rem - ty * F.nyz;
+    const int x0 = tx * kFusedTileX, y0 = ty * TT, z0 = tz * TT;
+    const int tri = A.triples[t];
+    const int fa = tri & 0xff, fb = (tri >> 8) & 0xff, fc = tri >> 16;
+    double *b0 = buf, *b1 = buf + 256, *b2 = buf + 512, *sig = buf + 768;
+    const bool dz = A.d_zero != 0;
+    if (lane == 0 && !dz) {
+        mbar_expect_tx(mbar, 3u * 256u * 8u);
+        tma_load_4d(b0, xa, z0, y0, x0, t, mbar);               // [x:4][y:8][z:8]
+        tma_load_4d(b1, xa, y0, z0, x0, g.ntri + t, mbar);      // [x:4][z:8][y:8]
+        tma_load_4d(b2, xb, x0, z0, y0, 2 * g.ntri + t, mbar);  // [y:8][z:8][x:4]
+    }
+    // sigma of the members' blocks: (x,y) 32, (x,z) 32, (y,z) 64
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+        const int e = lane + 32 * h;
+        int vw, u, w;
+        if (e < 32) { vw = 0; u = x0 + (e >> 3); w = y0 + (e & 7); }
+        else if (e < 64) { vw = 1; u = x0 + ((e - 32) >> 3); w = z0 + (e & 7); }
+        else { vw = 2; u = y0 + ((e - 64) >> 3); w = z0 + (e & 7); }
+        const int f = vw == 2 ? fb : fa, hh = vw == 0 ? fb : fc;
+        double sg = 0.0;
+        if (u < n && w < n && u != w)
+            sg = A.sigma[(unsigned)g.off[f] + (unsigned)(u * (n1 - f) * n1 + (hh - f - 1) * n1 + (w - (w > u)))];
+        sig[e] = sg;
+    }
+    __syncwarp();
+    if (!dz) {
+        mbar_wait(mbar, phase);
+        phase ^= 1;
+    }
+#pragma unroll
+    for (int h = 0; h < 8; h++) {
+        const int e = lane + 32 * h;
+        const int u = e >> 6, v = (e >> 3) & 7, w = e & 7;
+        const int x = x0 + u, y = y0 + v, z = z0 + w;
+        if (x < n && y < n && z < n && x != y && x != z && y != z) {
+            const int p0 = (u * TT + v) * TT + w, p1 = (u * TT + w) * TT + v, p2 = (v * TT + w) * kFusedTileX + u;
+            const double e1 = (dz ? 0.0 : b0[p0]) + sig[u * TT + v];
+            const double e2 = (dz ? 0.0 : b1[p1]) + sig[32 + u * TT + w];
+            const double e3 = (dz ? 0.0 : b2[p2]) + sig[64 + v * TT + w];
+            const double mu = div3((e1 + e2) + e3);
+            b0[p0] = mu;
+            b1[p1] = mu;
+            b2[p2] = mu;
+        }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_4d(xa, z0, y0, x0, t, b0);
+        tma_store_4d(xa, y0, z0, x0, g.ntri + t, b1);
+        tma_store_4d(xb, x0, z0, y0, 2 * g.ntri + t, b2);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        bulk_wait_all();  // written (not only read): the tile is published below
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        atomicAdd(&A.sched->done[fa], 1u);
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(1024, 1) k_fused_x(const FusedArgs F, const __grid_constant__ CUtensorMap xrow,
+                                                     const __grid_constant__ CUtensorMap xa,
+                                                     const __grid_constant__ CUtensorMap xb)
+{
+    const LapArgs &a = F.L;
+    if (__shfl_sync(FULL_MASK, a.ctl->stopped, 0)) return;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int wpc = blockDim.x >> 5, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0),
+              lane = threadIdx.x & 31;
+    const int col0 = 31 - lane;
+    const Geom &g = a.g;
+    const int n = g.n, m = a.m, m4 = (m + 3) & ~3, ldm = (n + 5) & ~3, np = g.np;
+    double *const buf = reinterpret_cast<double *>(smem + (size_t)warp * F.wbytes);
+    uint64_t *const mbar = reinterpret_cast<uint64_t *>(smem + (size_t)wpc * F.wbytes + (size_t)warp * 16);
+    double *const xurow = buf + n, *const xsel = xurow + 1;
+    Sched *const sc = a.sched;
+    if (lane == 0) {
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    uint32_t phase = 0;
+    int ready = -1;  // every triple with smallest facility <= ready is published
+    int icur = 0;
+    long long lb = 0, lend = 0, tb = 0, tend = 0;
+    bool t_out = false, l_out = false, anybad = false;
+    const bool prefer_t = (warp & F.tmask) == 0;
+    const long long CH = 4;
+    // lane 0 polls the published counters; the result is broadcast
+    auto is_ready = [&](int f) -> bool {
+        const int need = f < n - 3 ? f : n - 3;
+        int r = ready;
+        if (lane == 0) {
+            while (r < need) {
+                const int x = r + 1;
+                const unsigned total = (unsigned)F.tpt * (unsigned)((n - 1 - x) * (n - 2 - x) / 2);
+                if (ld_acquire(&sc->done[x]) >= total) r++;
+                else break;
+            }
+        }
+        ready = __shfl_sync(FULL_MASK, r, 0);
+        return ready >= need;
+    };
+    auto grab_l = [&]() {
+        long long c0 = 0;
+        if (lane == 0) c0 = (long long)atomicAdd(&sc->head, (unsigned long long)CH);
+        lb = __shfl_sync(FULL_MASK, c0, 0);
+        lend = lb + CH < a.count ? lb + CH : a.count;
+        if (lb >= a.count) l_out = true;
+    };
+    auto grab_t = [&]() {
+        long long c0 = 0;
+        if (lane == 0) c0 = (long long)atomicAdd(&sc->thead, (unsigned long long)CH);
+        tb = __shfl_sync(FULL_MASK, c0, 0);
+        tend = tb + CH < F.ntiles ? tb + CH : F.ntiles;
+        if (tb >= F.ntiles) t_out = true;
+    };
+    auto lap_job = [&](long long b) {
+        const unsigned ijkl = decode_l2(a, b, icur);
+        unsigned xr[1];
+        x_rows<1>(g, ijkl, m, lane, xr);
+        if (lane == 0) {
+            fence_proxy_async_global();  // published generic-side order -> our TMA reads
+            mbar_expect_tx(mbar, (uint32_t)(m4 * ldm * 8));
+        }
+        x_rows4<true>(&xrow, buf, ldm, m4, xr[0], lane, mbar);
+        mbar_wait(mbar, phase);
+        phase ^= 1;
+        const int j = (ijkl >> 8) & 0xff, l = ijkl >> 24;
+        int cofs[1] = {col0 < m ? x_col(col0, j, l) : j};
+        int poff[1], p[1], steps = 0;
+        double v[1], ucol[1];
+        warp_lap_solve1<false>(buf + cofs[0], m, ldm, lane, poff[0], v[0], ucol[0], steps);
+        bool bad;
+        const double *X = a.X;
+        const double S = warp_lap_epilogue<1>(
+            buf,
+            [&](int r, int t, int c) {
+                const double *src = X + (size_t)x_pick<1>(xr, r) * (size_t)np + cofs[t];
+                return c < m ? *src : 0.0;
+            },
+            m, ldm, cofs, lane, col0, poff, p, v, ucol, xurow, xsel, ldm, bad);
+        anybad |= bad;
+        x_rows4<false>(&xrow, buf, ldm, m4, xr[0], lane, mbar);
+        if (lane == 0) {
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            const int i = ijkl & 0xff, k = (ijkl >> 16) & 0xff, n1 = n - 1;
+            a.C[(int64_t)(i * n + j) * g.ldc + (k - 1) * n1 + (l - (l > j))] = S;  // reading R12
+            a.C[(int64_t)(k * n + l) * g.ldc + i * n1 + (j - (j > l))] = S;
+            bulk_wait_read();  // the buffer is free once the stores have read it
+        }
+        __syncwarp();
+    };
+    for (;;) {
+        if (tb < tend) {  // tiles already taken are finished first (others may wait on them)
+            fused_transfer_tile(F, tb++, buf, mbar, phase, lane, &xa, &xb);
+            continue;
+        }
+        if (!(prefer_t && !t_out)) {  // LAP first (one warp in four: transfer first)
+            if (lb >= lend && !l_out) grab_l();
+            if (lb < lend && is_ready(facility_of(g, lb, icur))) {
+                lap_job(lb++);
+                continue;
+            }
+        }
+        if (!t_out) {
+            grab_t();
+            if (tb < tend) continue;
+        }
+        // no transfer tile left: LAPs only (waiting for the tiles still in flight)
+        if (lb >= lend && !l_out) grab_l();
+        if (lb >= lend) break;
+        unsigned spins = 0;
+        while (!is_ready(facility_of(g, lb, icur))) {
+            __nanosleep(256);
+            if (++spins > (1u << 26)) __trap();  // ~20 s without progress: fail, never hang
+        }
+        lap_job(lb++);
+    }
+    if (lane == 0) bulk_wait_all();
+    if (anybad && lane == 0) atomicOr(&a.ctl->err, 1);
+}
+
+cudaError_t launch_fused_x(const Geom &g, const TransferArgs &A, double *X, double *C, Ctl *ctl, Sched *sched,
+                           int num_sms, const CUtensorMap &xa, const CUtensorMap &xb, const CUtensorMap &xrow,
+                           cudaStream_t st)
+{
+    const int n = g.n, m = n - 2;
+    if (m > 32 || n < kXMin) return cudaErrorInvalidValue;
+    FusedArgs F{};
+    LapArgs &a = F.L;
+    a.lvl = LAP_L2;
+    a.g = g;
+    a.m = m;
+    a.count = g.nblk;
+    a.ld = g.ld2;
+    a.C = C;
+    a.ctl = ctl;
+    a.X = X;
+    a.sched = sched;
+    a.mag_n1 = (uint32_t)((0x100000000ull + (uint64_t)(n - 2)) / (uint64_t)(n - 1));
+    for (int i = 0; i + 1 < n; i++) {
+        const uint64_t d = (uint64_t)(n - 1 - i) * (uint64_t)(n - 1);
+        a.mag_pj[i] = (uint32_t)((0x100000000ull + d - 1) / d);
+    }
+    F.T = A;
+    F.ntx = (n + kFusedTileX - 1) / kFusedTileX;
+    F.nyz = (n + TT - 1) / TT;
+    F.tpt = F.ntx * F.nyz * F.nyz;
+    F.ntiles = (long long)F.tpt * g.ntri;
+    const int ldm = (n + 5) & ~3;
+    size_t lapb = (size_t)((m + 3) & ~3) * ldm * 8;
+    size_t wb = lapb > 7168 ? lapb : 7168;  // a transfer tile needs 3 x 2 KB boxes + 1 KB sigma
+    wb = (wb + 1023) & ~size_t(1023);
+    F.wbytes = (int)wb;
+    F.tmask = 3;  // one warp in four prefers transfer tiles (QAP_FUSED_TMASK: experiment knob)
+    if (const char *ev = getenv("QAP_FUSED_TMASK")) F.tmask = atoi(ev);
+    int wpc = 32;
+    while (wpc > 1 && (wb + 16) * wpc > (size_t)226 * 1024) wpc--;
+    const size_t smem = (wb + 16) * wpc;
+    static std::mutex mu;
+    static uint64_t done_dev = 0;
+    {
+        int dev = 0;
+        cudaError_t e0 = cudaGetDevice(&dev);
+        if (e0 != cudaSuccess) return e0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 64 || !((done_dev >> dev) & 1)) {
+            int mx = 0;
+            if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+                return e0;
+            if ((e0 = cudaFuncSetAttribute(k_fused_x, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
+                cudaSuccess)
+                return e0;
+            if (dev < 64) done_dev |= 1ull << dev;
+        }
+    }
+    k_fused_x<<<num_sms, 32 * wpc, smem, st>>>(F, xrow, xa, xb);
     return cudaGetLastError();
 }
 

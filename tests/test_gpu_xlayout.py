@@ -94,3 +94,15 @@ def test_fold_from_class_layout_parent(orc, pkg):
         compare_state(pkg, hc, sc)
     pkg.qap_destroy(hp)
     pkg.qap_destroy(hc)
+
+
+@pytest.mark.parametrize("family,n,fixed,T", [("nug", 16, (), 3), ("taib", 17, ((3, 3),), 2), ("nug", 24, (), 2),
+                                              ("nug", 30, (), 2), ("taib", 33, (), 1)])
+def test_fused_iteration_equals_separate_kernels(pkg, family, n, fixed, T):
+    """QAP_FLAG_FUSED (transfer tiles and level-2 LAPs in one persistent kernel, LAPs gated
+    by per-facility completion counters) leaves the same dual state bit for bit."""
+    inst = qapgen.make(family, n, 5)
+    ra, Ba, Ca, Da, la = _state(pkg, n, inst, 0, fixed, T)
+    rb, Bb, Cb, Db, lb_ = _state(pkg, n, inst, pkg.QAP_FLAG_FUSED, fixed, T)
+    assert la == lb_ and (ra["trace"] == rb["trace"]).all()
+    assert (Ba == Bb).all() and (Ca == Cb).all() and np.array_equal(Da, Db)
