@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--lap-warps", type=int, default=0)
     ap.add_argument("--no-bnb", action="store_true")
     ap.add_argument("--fused", action="store_true", help="QAP_FLAG_FUSED: transfer + level-2 LAPs in one kernel")
+    ap.add_argument("--class-layout", action="store_true", help="QAP_FLAG_CLASS_LAYOUT (A/B of the level-2 layouts)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded bound")
     args = ap.parse_args()
 
@@ -211,7 +212,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     n, T = args.n, T_ITERS
     inst = qapgen.nug(n, SEED)
-    FL = pkg.QAP_FLAG_TIME_KERNELS | (pkg.QAP_FLAG_FUSED if args.fused else 0)
+    FL = (pkg.QAP_FLAG_TIME_KERNELS | (pkg.QAP_FLAG_FUSED if args.fused else 0)
+          | (pkg.QAP_FLAG_CLASS_LAYOUT if args.class_layout or args.fused else 0))
     stream = torch.cuda.current_stream()
     sharded, shard_err = False, None
     if world > 1 and not args.replicas:
@@ -384,7 +386,7 @@ def main():
         alg_bytes = 16 * shard_entries
     dom = max(("lap2", "transfer"), key=lambda k: per.get(k, {}).get("share", 0))
     achieved = alg_bytes / (per[dom]["avg_ms"] / 1e3) / 1e9
-    xl = (not sharded) and n >= 16     # class layout of the level-2 dual
+    xl = (not sharded) and n >= 16 and (args.class_layout or args.fused)  # class layout
     fused = xl and args.fused and "transfer" not in per
     names = {"lap2": "k_fused_x (transfer + level-2 concentration in one persistent kernel, class layout)" if fused
              else "k_lap<1,1,0,1> (level-2 concentration, class layout, TMA gather4/scatter4)" if xl

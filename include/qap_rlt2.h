@@ -68,14 +68,15 @@ typedef struct {
                                      internal streams (experimental; default: one after the other) */
 #define QAP_FLAG_NO_GRAPH 4       /* do not replay the iteration loop from a cached CUDA graph     */
 #define QAP_FLAG_LDG_TRANSFER 8   /* transfer with per-element loads instead of tensor-map TMA    */
-#define QAP_FLAG_BLOCK_LAYOUT 16  /* keep the level-2 dual in the stored-block layout at every node
-                                     size (default: nodes with n >= 16 are bounded in the class
-                                     layout of DESIGN.md §6; results are bit-identical either way,
-                                     and qap_rlt2_dual_copy always exports the block layout)      */
-#define QAP_FLAG_FUSED 32         /* class layout, one column per lane (16 <= n <= 34): run each
-                                     iteration's transfer and level-2 LAPs as ONE persistent
-                                     kernel (warps take transfer tiles or LAPs whose facility is
-                                     transferred; bit-identical results)                         */
+#define QAP_FLAG_CLASS_LAYOUT 16  /* bound nodes with n >= 16 in the class layout of DESIGN.md §6
+                                     (per-member arrays: the transfer moves dense TMA boxes, the
+                                     level-2 LAP gathers its rows with TMA gather4/scatter4);
+                                     bit-identical results; default: the stored-block layout.
+                                     qap_rlt2_dual_copy always exports the block layout          */
+#define QAP_FLAG_FUSED 32         /* with QAP_FLAG_CLASS_LAYOUT, 16 <= n <= 34: each iteration's
+                                     transfer and level-2 LAPs as ONE persistent kernel (warps take
+                                     transfer tiles or LAPs whose facility is transferred);
+                                     experimental, bit-identical, measured slower */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */

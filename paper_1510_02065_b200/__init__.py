@@ -27,7 +27,7 @@ QAP_FLAG_TIME_KERNELS = 1
 QAP_FLAG_OVERLAP = 2
 QAP_FLAG_NO_GRAPH = 4
 QAP_FLAG_LDG_TRANSFER = 8
-QAP_FLAG_BLOCK_LAYOUT = 16
+QAP_FLAG_CLASS_LAYOUT = 16
 QAP_FLAG_FUSED = 32
 PHASE_ITER0, PHASE_TRANSFER, PHASE_CONC_D, PHASE_CONC_C, PHASE_CONC_B = range(5)
 KERNEL_KINDS = ["init", "sigma", "transfer", "lap2", "lap1", "lap0"]

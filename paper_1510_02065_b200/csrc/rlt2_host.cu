@@ -89,8 +89,9 @@ struct qap_rlt2 {
     // tensor maps of D for k_transfer_tma, encoded for node size tma_n (0: none / failed)
     TmaMaps tma{};
     int tma_n = 0;
-    // class layout X of the level-2 dual: allocated for n_cap >= kXMin on
-    // single-rank handles; the block buffer dD is then allocated on first need (bytesD).
+    // class layout X of the level-2 dual (QAP_FLAG_CLASS_LAYOUT): allocated for
+    // n_cap >= kXMin on single-rank handles; the block buffer dD is then allocated on first
+    // need (bytesD).
     // dvalid: bit 0 = dD holds the current D, bit 1 = dX does (both while D is lazily zero).
     double *dX = nullptr;
     size_t bytesD = 0;
@@ -294,9 +295,9 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         delete h;
         return s;
     }
-    // class layout unless the flags pin the block-layout kernels
-    const bool xl = world == 1 && !loopback && h->n_cap >= kXMin &&
-                    !(h->flags & (QAP_FLAG_BLOCK_LAYOUT | QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER));
+    // class layout when asked for and compatible with the other flags
+    const bool xl = world == 1 && !loopback && h->n_cap >= kXMin && (h->flags & QAP_FLAG_CLASS_LAYOUT) &&
+                    !(h->flags & (QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER));
     const size_t bytesX = xl ? x_doubles(h->n_cap) * 8 : 0;
     h->bytesD = bytesD;
     const size_t need = (xl ? bytesX : bytesD) + bytesC + bytesB + bytesS + (64u << 20);
@@ -676,7 +677,8 @@ static bool x_map(qap_rlt2 *h)
 static bool use_x(qap_rlt2 *h)
 {
     return h->dX && h->world == 1 && !h->loopback && h->geom.n >= kXMin &&
-           !(h->flags & (QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER | QAP_FLAG_BLOCK_LAYOUT)) && x_map(h);
+           (h->flags & QAP_FLAG_CLASS_LAYOUT) && !(h->flags & (QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER)) &&
+           x_map(h);
 }
 static qap_status ensure_dD(qap_rlt2 *h)
 {

@@ -1,6 +1,6 @@
-"""GPU: the class layout of the level-2 dual (default for nodes with n >= 16)
-runs the same per-class and per-block operations as the stored-block layout
-(QAP_FLAG_BLOCK_LAYOUT), so whole dual states are bit-identical between the two — after
+"""GPU: the class layout of the level-2 dual (QAP_FLAG_CLASS_LAYOUT, nodes with
+n >= 16) runs the same per-class and per-block operations as the default stored-block
+layout, so whole dual states are bit-identical between the two — after
 bounds at the root and at fixed nodes, for even and odd n (odd n pads the innermost
 stride), for one and two columns per lane (n - 2 > 32), phase by phase against the
 oracle, across exports in the middle of an iteration, and for warm children folded from
@@ -38,8 +38,8 @@ def _state(pkg, n, inst, flags, fixed, T):
                                               ("taib", 35, (), 1)])
 def test_class_layout_equals_block_layout(pkg, family, n, fixed, T):
     inst = qapgen.make(family, n, 3)
-    ra, Ba, Ca, Da, la = _state(pkg, n, inst, 0, fixed, T)
-    rb, Bb, Cb, Db, lb_ = _state(pkg, n, inst, pkg.QAP_FLAG_BLOCK_LAYOUT, fixed, T)
+    ra, Ba, Ca, Da, la = _state(pkg, n, inst, pkg.QAP_FLAG_CLASS_LAYOUT, fixed, T)
+    rb, Bb, Cb, Db, lb_ = _state(pkg, n, inst, 0, fixed, T)
     assert la == lb_ and (ra["trace"] == rb["trace"]).all() and ra["lb_glb"] == rb["lb_glb"]
     assert (Ba == Bb).all() and (Ca == Cb).all() and np.array_equal(Da, Db)
 
@@ -49,7 +49,7 @@ def test_phase_by_phase_class_layout(orc, pkg, family, n):
     """Every phase of Algorithm 1 in the class layout leaves the oracle's B, C,
     D, LB (each export converts the class layout to stored blocks)."""
     inst = qapgen.make(family, n, 2)
-    h = pkg.qap_rlt2_create(n, inst.F, inst.D)
+    h = pkg.qap_rlt2_create(n, inst.F, inst.D, flags=pkg.QAP_FLAG_CLASS_LAYOUT)
     st = orc.State(inst.F, inst.D)
     pkg.qap_rlt2_step(h, pkg.PHASE_ITER0)
     st.iteration0()
@@ -80,8 +80,8 @@ def test_fold_from_class_layout_parent(orc, pkg):
     bound (class layout again), equal the oracle bit for bit."""
     n = 17
     inst = qapgen.taib(n, 4)
-    hp = pkg.qap_rlt2_create(n, inst.F, inst.D)
-    hc = pkg.qap_rlt2_create(n, inst.F, inst.D)
+    hp = pkg.qap_rlt2_create(n, inst.F, inst.D, flags=pkg.QAP_FLAG_CLASS_LAYOUT)
+    hc = pkg.qap_rlt2_create(n, inst.F, inst.D, flags=pkg.QAP_FLAG_CLASS_LAYOUT)
     sp = orc.State(inst.F, inst.D)
     assert pkg.qap_rlt2_bound(hp, 2)["lb"] == sp.bound(2)["lb"]
     I, J = sp.free_maps()
@@ -103,6 +103,6 @@ def test_fused_iteration_equals_separate_kernels(pkg, family, n, fixed, T):
     by per-facility completion counters) leaves the same dual state bit for bit."""
     inst = qapgen.make(family, n, 5)
     ra, Ba, Ca, Da, la = _state(pkg, n, inst, 0, fixed, T)
-    rb, Bb, Cb, Db, lb_ = _state(pkg, n, inst, pkg.QAP_FLAG_FUSED, fixed, T)
+    rb, Bb, Cb, Db, lb_ = _state(pkg, n, inst, pkg.QAP_FLAG_FUSED | pkg.QAP_FLAG_CLASS_LAYOUT, fixed, T)
     assert la == lb_ and (ra["trace"] == rb["trace"]).all()
     assert (Ba == Bb).all() and (Ca == Cb).all() and np.array_equal(Da, Db)
