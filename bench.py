@@ -403,7 +403,9 @@ def main():
         roof["issue"] = {"warp_inst_per_launch": ins, "issue_slots_per_launch": slots, "frac": ins / slots,
                          "source": "instructions: committed ncu capture (profiles/traffic.json); slots: "
                                    "4 schedulers x SMs x median SM clock x live CUDA-event duration",
-                         "note": "the level-2 LAP kernel is bound by warp-instruction issue, not by HBM"}
+                         "note": "the level-2 LAP kernel is bound by its dependent Dijkstra chain at 32 warps/SM "
+                                 "(shared memory caps the warps): issue, not HBM; instructions = mean over the "
+                                 "ascent's iterations"}
     other = "transfer" if dom == "lap2" else "lap2"
     if other in per:  # the other D kernel against the same roofline (the transfer is HBM-bound)
         a2 = alg_bytes / (per[other]["avg_ms"] / 1e3) / 1e9
