@@ -89,3 +89,20 @@ def test_product_does_not_reference_oracle():
             if f.endswith((".py", ".cu", ".h", ".cuh", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt and "rlt2_oracle" not in txt, f
+
+
+def test_flag_constants_match_header(pkg):
+    src = open(os.path.join(ROOT, "include", "qap_rlt2.h")).read()
+    flags = dict(re.findall(r"#define\s+(QAP_FLAG_[A-Z_]+)\s+(\d+)", src))
+    assert flags, "no QAP_FLAG_* in the header"
+    for name, val in flags.items():
+        assert getattr(pkg, name) == int(val), name
+
+
+def test_tensor_tma_in_sass(pkg):
+    """The transfers move boxes with tensor-map TMA; the class-layout LAP gathers rows with
+    tile::gather4 / tile::scatter4 (sm_100a)."""
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", pkg.LIB_PATH],
+                          capture_output=True, text=True).stdout
+    assert "UTMALDG.4D" in sass and "UTMASTG.4D" in sass
+    assert "UTMALDG.2D.GATHER4" in sass and "UTMASTG.2D.SCATTER4" in sass
