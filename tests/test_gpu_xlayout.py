@@ -106,3 +106,21 @@ def test_fused_iteration_equals_separate_kernels(pkg, family, n, fixed, T):
     rb, Bb, Cb, Db, lb_ = _state(pkg, n, inst, pkg.QAP_FLAG_FUSED | pkg.QAP_FLAG_CLASS_LAYOUT, fixed, T)
     assert la == lb_ and (ra["trace"] == rb["trace"]).all()
     assert (Ba == Bb).all() and (Ca == Cb).all() and np.array_equal(Da, Db)
+
+
+@pytest.mark.parametrize("warm", [False, True])
+def test_bnb_with_class_layout_root(pkg, warm):
+    """A B&B whose root (n = 16) is bounded in the class layout and whose children (n <= 15)
+    in the block layout — cold children, or warm ones folded / copied from class-layout
+    states — takes the same decisions as the block-layout search: optimum, permutation and
+    node counts."""
+    inst = qapgen.nug(16, 3)
+    out = []
+    for fl in (0, pkg.QAP_FLAG_CLASS_LAYOUT):
+        h = pkg.qap_rlt2_create(16, inst.F, inst.D, flags=fl)
+        r = pkg.qap_bnb_solve(h, 2, batch=4, warm=warm)
+        out.append(r)
+        pkg.qap_destroy(h)
+    a, b = out
+    assert a["opt"] == b["opt"] and (np.asarray(a["perm"]) == np.asarray(b["perm"])).all()
+    assert a["bounded"] == b["bounded"] and a["leaves"] == b["leaves"]
