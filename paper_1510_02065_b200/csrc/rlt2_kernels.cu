@@ -151,14 +151,6 @@ __device__ __forceinline__ int x_rowfac(int r, int i, int k)
     return p + (p >= k);
 }
 
-__device__ __forceinline__ void cp_async8(void *dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_wait()
-{
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -520,18 +512,9 @@ struct LapArgs {
     const CUtensorMap *xrow;  // host: 2-D map [3 ntri n n][np] of X with {np, 1} boxes (gather4)
 };
 // TMA tile::gather4 / tile::scatter4 (sm_100a): four row runs of X <-> four consecutive
-// rows of the cost buffer in one instruction (2-D map, box {np, 1}; coordinates {0, rows})
-__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, unsigned r0, unsigned r1, unsigned r2,
-                                            unsigned r3, uint64_t *mbar)
-{
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-        "%4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(mbar))
-        : "memory");
-}
-// all row groups of one block: lane 0 issues one gather4 (load) or scatter4 (store) per 4
-// rows; row r's run index is held by lane r (x_rows), rows >= m by junk row 0
+// rows of the cost buffer in one instruction (2-D row map, box {ldm, 1}, coordinates
+// {0, rows}).  All row groups of one block: lane 0 issues one gather4 (load) or scatter4
+// (store) per 4 rows; row r's run index is held by lane r (x_rows), rows >= m by junk row 0.
 template <bool LOAD>
 __device__ __forceinline__ void x_rows4(const CUtensorMap *tm, double *M, int ldm, int m4, unsigned xr, int lane,
                                         uint64_t *mbar)
@@ -560,15 +543,6 @@ __device__ __forceinline__ void x_rows4(const CUtensorMap *tm, double *M, int ld
         }
         sa += gstep;
     }
-}
-__device__ __forceinline__ void tma_scatter4(const CUtensorMap *tm, unsigned r0, unsigned r1, unsigned r2, unsigned r3,
-                                             const void *src)
-{
-    asm volatile(
-        "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
-            reinterpret_cast<uint64_t>(tm)),
-        "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(src))
-        : "memory");
 }
 
 // Level 2: pairs (i,j), (k,l) of stored block b (i = canonical first facility; `icur` is a
