@@ -325,6 +325,17 @@ __device__ __noinline__ uint32_t tie_low_word(double minv, uint32_t sg, uint32_t
     const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
     return __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
 }
+// the argmin's ballot through the full order-preserving key (some minv is negative or -0)
+__device__ __noinline__ uint32_t argmin_keyed(double minv)
+{
+    const uint32_t hb = static_cast<uint32_t>(__double2hiint(minv));
+    const uint32_t sg = static_cast<uint32_t>(static_cast<int32_t>(hb) >> 31);
+    const uint32_t hi = hb ^ (sg | 0x80000000u);
+    const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
+    uint32_t bal = __ballot_sync(FULL_MASK, hi == mhi);
+    if (bal & (bal - 1u)) bal = tie_low_word(minv, sg, hi, mhi);
+    return bal;
+}
 template <bool COUNT>
 __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int ldm, int lane, int &poff, double &v,
                                                 double &ucol, int &steps)
@@ -347,13 +358,16 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
                 minv = cur;
                 way = j0;
             }
-            // argmin of (minv, matched?, column): high word of the order key first
-            const uint32_t hb = static_cast<uint32_t>(__double2hiint(minv));
-            const uint32_t sg = static_cast<uint32_t>(static_cast<int32_t>(hb) >> 31);
-            const uint32_t hi = hb ^ (sg | 0x80000000u);
-            const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
-            uint32_t bal = __ballot_sync(FULL_MASK, hi == mhi);
-            if (bal & (bal - 1u)) bal = tie_low_word(minv, sg, hi, mhi);
+            // argmin of (minv, matched?, column).  While no minv is negative (Dijkstra
+            // distances are >= 0 up to rounding; settled columns hold +NaN) the raw high words
+            // order the values as signed integers (and equal high words by their low words as
+            // unsigned): one signed redux on the common path; a negative minimum (a negative
+            // value or -0 somewhere) takes the order-preserving key (warp-uniform branch).
+            const int32_t hs = __double2hiint(minv);
+            const int32_t mhs = __reduce_min_sync(FULL_MASK, hs);
+            uint32_t bal = __ballot_sync(FULL_MASK, hs == mhs);
+            if (mhs < 0) bal = argmin_keyed(minv);
+            else if (bal & (bal - 1u)) bal = tie_low_word(minv, 0u, (uint32_t)hs, (uint32_t)mhs);
             const uint32_t ft = bal & freemask;
             j1 = 31 - __clz(ft ? ft : bal);  // highest lane = lowest column
             const double delta = __shfl_sync(FULL_MASK, minv, j1);
