@@ -325,6 +325,13 @@ __device__ __noinline__ uint32_t tie_low_word(double minv, uint32_t sg, uint32_t
     const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
     return __ballot_sync(FULL_MASK, hi == mhi && lo == mlo);
 }
+// index of the highest set bit (bfind: one FLO, so that merged values stay FLO results)
+__device__ __forceinline__ int hibit(uint32_t x)
+{
+    int r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
 // the argmin's ballot through the full order-preserving key (some minv is negative or -0)
 __device__ __noinline__ uint32_t argmin_keyed(double minv)
 {
@@ -366,10 +373,13 @@ __device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int 
             const int32_t hs = __double2hiint(minv);
             const int32_t mhs = __reduce_min_sync(FULL_MASK, hs);
             uint32_t bal = __ballot_sync(FULL_MASK, hs == mhs);
-            if (mhs < 0) bal = argmin_keyed(minv);
-            else if (bal & (bal - 1u)) bal = tie_low_word(minv, 0u, (uint32_t)hs, (uint32_t)mhs);
+            j1 = hibit(bal);  // a unique minimum (the common case): the next column
+            if (mhs < 0 || (bal & (bal - 1u))) {  // several minima (or a negative one)
+                bal = mhs < 0 ? argmin_keyed(minv) : tie_low_word(minv, 0u, (uint32_t)hs, (uint32_t)mhs);
+                const uint32_t fb = bal & freemask;
+                j1 = hibit(fb ? fb : bal);  // a free column first; highest lane = lowest column
+            }
             const uint32_t ft = bal & freemask;
-            j1 = 31 - __clz(ft ? ft : bal);  // highest lane = lowest column
             const double delta = __shfl_sync(FULL_MASK, minv, j1);
             const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
             const double nx_u = __shfl_sync(FULL_MASK, ucol, j1);
