@@ -495,7 +495,10 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, GVal Mg, int m, i
 __host__ __device__ inline size_t lap_buf_bytes(int m, int cpl, int ldrow = 0)
 {
     if (ldrow > 0) return ((size_t)m * ldrow * 8 + 15) & ~size_t(15);
-    return (((size_t)m * m + 32 * cpl) * 8 + 15) & ~size_t(15);
+    // lanes without a column read entry (r, c >= m) of any row r: the block plus 32 cpl - m
+    // doubles of padding keeps every such read inside the buffer
+    const int pad = 32 * cpl > m ? 32 * cpl - m : 0;
+    return (((size_t)m * m + pad) * 8 + 15) & ~size_t(15);
 }
 __host__ __device__ inline size_t lap_warp_smem(int m, int cpl, int nbuf, int ldrow = 0)
 {
@@ -2121,10 +2124,23 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
     if (a.m > 64) return cudaErrorInvalidValue;
     const int nbuf = (lap_cfg & 0x100) ? 2 : 1;
     int wpc = lap_cfg & 0xff;
-    if (wpc <= 0) wpc = a.sched ? 32 : 8;
     int cps = (lap_cfg >> 12) & 0xf;
+    if (wpc <= 0 && a.sched && !a.X && a.ntile3 == 0) {
+        // default level-2 configuration: the most resident warps per SM that shared memory
+        // allows (228 KB per SM, 1 KB reserved per CTA), e.g. 2 CTAs x 17 warps at m = 28
+        const size_t ws = lap_warp_smem(a.m, cpl, nbuf);
+        int best = 0;
+        for (int c = 1; c <= 2; c++)
+            for (int w = 32; w >= 1; w--)
+                if ((size_t)c * (w * ws + 1024) <= 233472 && w * c <= 42 && w * c > best) {
+                    best = w * c;
+                    wpc = w;
+                    cps = c;
+                }
+    }
+    if (wpc <= 0) wpc = a.sched ? 32 : 8;
     if (cps <= 0) cps = 1;
-    const size_t cap = (size_t)226 * 1024 / (a.sched ? cps : 1);
+    const size_t cap = a.sched ? (size_t)233472 / cps - 1024 : (size_t)226 * 1024;
     const int ldrow = (a.X && cpl == 1) ? ((a.g.n + 5) & ~3) : 0;
     while (wpc > 1 && lap_warp_smem(a.m, cpl, nbuf, ldrow) * wpc > cap) wpc--;
     if (a.X) {  // class layout (no overlap mode, single buffer)
