@@ -187,10 +187,19 @@ __device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const int
         }
         const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
         const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
-        const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
-        const bool tie = (hi == mhi) && (lo == mlo);
-        const uint32_t mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
-        const uint32_t pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
+        const uint32_t hb = __ballot_sync(FULL_MASK, hi == mhi);
+        uint32_t mlo, mr, pick;
+        if (hb & (hb - 1u)) {  // several lanes share the minimal high word: low words, then rank
+            mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
+            const bool tie = (hi == mhi) && (lo == mlo);
+            mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
+            pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
+        } else {  // one lane holds the minimum (its lane-local pick already applied the rank)
+            const int w = __ffs(hb) - 1;
+            mlo = __shfl_sync(FULL_MASK, lo, w);
+            mr = static_cast<uint32_t>(__shfl_sync(FULL_MASK, rank, w));
+            pick = hb;
+        }
         const int t = static_cast<int>(mr) % CPL;
         j1 = (__ffs(pick) - 1) + 32 * t;
         j1free = static_cast<int>(mr) < CPL;
