@@ -167,44 +167,79 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+// Argmin over the two columns of every lane by (value, matched?, column), through the full
+// order-preserving key: exact for every value (negatives, -0).  Out of line: taken only when
+// some candidate is negative.
+struct ArgMin2 {
+    int j1;
+    int free;
+    double delta;
+};
+__device__ __noinline__ ArgMin2 warp_argmin_keyed2(double m0, double m1, int p0, int p1)
+{
+    uint64_t key = okey(m0);
+    int rank = (p0 >= 0 ? 2 : 0);
+    const uint64_t k1 = okey(m1);
+    const int r1 = (p1 >= 0 ? 2 : 0) + 1;
+    if (k1 < key || (k1 == key && r1 < rank)) {
+        key = k1;
+        rank = r1;
+    }
+    const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
+    const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
+    const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
+    const bool tie = (hi == mhi) && (lo == mlo);
+    const uint32_t mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
+    const uint32_t pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
+    ArgMin2 r;
+    r.j1 = (__ffs(pick) - 1) + 32 * (static_cast<int>(mr) % 2);
+    r.free = static_cast<int>(mr) < 2;
+    r.delta = okey_inv((static_cast<uint64_t>(mhi) << 32) | mlo);
+    return r;
+}
+
+// Two columns per lane (m in (32, 64]).  While no candidate is negative (Dijkstra distances
+// are >= 0 up to rounding; settled columns hold +NaN) the raw bits order the values as signed
+// 64-bit integers: the lane-local pick compares raw bits (a negative candidate always wins it,
+// so a negative anywhere shows up as a negative minimal high word and takes the keyed path),
+// the warp-wide pick is one signed redux on the high words, and a minimum held by one lane is
+// read from it by shuffle.
 template <int CPL>
 __device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const int (&poff)[CPL], int &j1, bool &j1free,
                                             double &delta)
 {
-    static_assert(CPL > 1, "CPL == 1 uses warp_lap_solve1");
-    {
-        // lane-local best by (key, matched, t), then warp-wide
-        uint64_t key = ~0ull;
-        int rank = 0xff;
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            const uint64_t k = okey(minv[t]);
-            const int r = (poff[t] >= 0 ? CPL : 0) + t;
-            if (k < key || (k == key && r < rank)) {
-                key = k;
-                rank = r;
-            }
-        }
-        const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
-        const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
-        const uint32_t hb = __ballot_sync(FULL_MASK, hi == mhi);
-        uint32_t mlo, mr, pick;
-        if (hb & (hb - 1u)) {  // several lanes share the minimal high word: low words, then rank
-            mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
-            const bool tie = (hi == mhi) && (lo == mlo);
-            mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
-            pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
-        } else {  // one lane holds the minimum (its lane-local pick already applied the rank)
-            const int w = __ffs(hb) - 1;
-            mlo = __shfl_sync(FULL_MASK, lo, w);
-            mr = static_cast<uint32_t>(__shfl_sync(FULL_MASK, rank, w));
-            pick = hb;
-        }
-        const int t = static_cast<int>(mr) % CPL;
-        j1 = (__ffs(pick) - 1) + 32 * t;
-        j1free = static_cast<int>(mr) < CPL;
-        delta = okey_inv((static_cast<uint64_t>(mhi) << 32) | mlo);
+    static_assert(CPL == 2, "CPL == 1 uses warp_lap_solve1; m <= 64");
+    const int64_t b0 = __double_as_longlong(minv[0]), b1 = __double_as_longlong(minv[1]);
+    const int r0 = (poff[0] >= 0 ? 2 : 0), r1 = (poff[1] >= 0 ? 2 : 0) + 1;
+    const bool p1 = b1 < b0 || (b1 == b0 && r1 < r0);
+    const int64_t kb = p1 ? b1 : b0;
+    const int rank = p1 ? r1 : r0;
+    const int32_t hs = static_cast<int32_t>(kb >> 32);
+    const uint32_t lo = static_cast<uint32_t>(kb);
+    const int32_t mhs = __reduce_min_sync(FULL_MASK, hs);
+    if (mhs < 0) {
+        const ArgMin2 r = warp_argmin_keyed2(minv[0], minv[1], poff[0], poff[1]);
+        j1 = r.j1;
+        j1free = r.free != 0;
+        delta = r.delta;
+        return;
     }
+    const uint32_t hb = __ballot_sync(FULL_MASK, hs == mhs);
+    uint32_t mlo, mr, pick;
+    if (hb & (hb - 1u)) {  // several lanes share the minimal high word: low words, then rank
+        mlo = __reduce_min_sync(FULL_MASK, hs == mhs ? lo : 0xffffffffu);
+        const bool tie = (hs == mhs) && (lo == mlo);
+        mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
+        pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
+    } else {  // one lane holds the minimum (its lane-local pick already applied the rank)
+        const int w = __ffs(hb) - 1;
+        mlo = __shfl_sync(FULL_MASK, lo, w);
+        mr = static_cast<uint32_t>(__shfl_sync(FULL_MASK, rank, w));
+        pick = hb;
+    }
+    j1 = (__ffs(pick) - 1) + 32 * (static_cast<int>(mr) % 2);
+    j1free = static_cast<int>(mr) < 2;
+    delta = __hiloint2double(mhs, static_cast<int>(mlo));
 }
 
 template <int CPL, class T>
