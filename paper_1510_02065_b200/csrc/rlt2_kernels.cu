@@ -1890,7 +1890,7 @@ __global__ void __launch_bounds__(1024, 1) k_fused_x(const FusedArgs F, const __
 {
     const LapArgs &a = F.L;
     if (__shfl_sync(FULL_MASK, a.ctl->stopped, 0)) return;
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];  // buffers at 1 KB multiples: boxes 128-byte aligned
     const int wpc = blockDim.x >> 5, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0),
               lane = threadIdx.x & 31;
     const int col0 = 31 - lane;
