@@ -1404,16 +1404,20 @@ __device__ __forceinline__ int box_pos(int vw, int j, int l, int q, int j0, int 
 
 // WIDE: the stored D has >= 2^32 entries (n >= 47): row offsets relative to 64-bit per-view
 // base blocks; otherwise absolute 32-bit element indices (fewer instructions).
-template <int BX0, bool WIDE>  // BX0 = TT + 2 (m2 even: window starts are even) or TT + 4
-__global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, const __grid_constant__ TmaMaps M)
+// NT = 256: each thread averages 2 classes, the means are parked in a per-class array (8 CTAs
+// per SM by threads); NT = 128: 4 classes per thread, the means are written over the members'
+// box slots and the store phase reads them from there (no mean array: 11 CTAs per SM).
+template <int BX0, bool WIDE, int NT>  // BX0 = TT + 2 (m2 even: window starts are even) or TT + 4
+__global__ void __launch_bounds__(NT, NT == 256 ? 8 : 11) k_transfer_tma(const TransferArgs A, const __grid_constant__ TmaMaps M)
 {
     constexpr int BOXE = TT * kBox1 * BX0;
+    constexpr bool INBOX = NT == 128;
     if (A.ctl->stopped) return;
     __shared__ __align__(128) double box[3][BOXE];
     // class (a,b,c) = (j-j0, l-l0, q-q0) -> its mean at a * MA + b * MB + c (odd strides:
     // the permuted reads of the store phase are bank-conflict free)
     constexpr int MB = TT + 1, MA = TT * MB + 1;
-    __shared__ double mean[TT * MA];
+    __shared__ double mean[INBOX ? 1 : TT * MA];
     __shared__ unsigned rbase[3][TT * TT];  // element offset of each view row from the view's base
     __shared__ double rsig[3][TT * TT];
     __shared__ __align__(8) uint64_t mbar;
@@ -1447,8 +1451,8 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
         tma_load_4d(box[2], &M.m[k], s2 - o2, q0 > 0 ? q0 - 1 : 0, p - k - 1, l0, &mbar);
     }
     // per view row: element index of the row in D (stores) and sigma of its block
-    if (tid < 3 * TT * TT) {
-        const int vw = tid >> 6, x = (tid >> 3) & 7, y = tid & 7;
+    for (int er = tid; er < 3 * TT * TT; er += NT) {
+        const int vw = er >> 6, x = (er >> 3) & 7, y = er & 7;
         int r0, r1;
         if (vw == 0) { r0 = j0 + x; r1 = l0 + y; }
         else if (vw == 1) { r0 = j0 + x; r1 = q0 + y; }
@@ -1469,44 +1473,52 @@ __global__ void __launch_bounds__(256, 8) k_transfer_tma(const TransferArgs A, c
                 base = bb * (unsigned)ld2 + (unsigned)(row * m2);
             }
         }
-        rbase[vw][tid & 63] = base;
-        rsig[vw][tid & 63] = sg;
+        rbase[vw][er & 63] = base;
+        rsig[vw][er & 63] = sg;
     }
     __syncthreads();
     if (!dz) mbar_wait(&mbar, 0);
     // mean of each class (j,l,q) of the tile: ((e1 + e2) + e3) / 3 with e = stored + sigma.
     // View 0's store element e is class e itself: stored from the register right away.
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-        const int e = tid + 256 * h;
+    for (int h = 0; h < TT * TT * TT / NT; h++) {
+        const int e = tid + NT * h;
         const int a = e >> 6, b = (e >> 3) & 7, c = e & 7;
         const int j = j0 + a, l = l0 + b, q = q0 + c;
         if (j < n && l < n && q < n && j != l && j != q && l != q) {
+            const int b1 = box_pos<BX0>(1, j, l, q, j0, l0, q0, o1), b2 = box_pos<BX0>(2, j, l, q, j0, l0, q0, o2);
             const double e1 = (dz ? 0.0 : box[0][box_pos<BX0>(0, j, l, q, j0, l0, q0, o0)]) + rsig[0][a * 8 + b];
-            const double e2 = (dz ? 0.0 : box[1][box_pos<BX0>(1, j, l, q, j0, l0, q0, o1)]) + rsig[1][a * 8 + c];
-            const double e3 = (dz ? 0.0 : box[2][box_pos<BX0>(2, j, l, q, j0, l0, q0, o2)]) + rsig[2][b * 8 + c];
+            const double e2 = (dz ? 0.0 : box[1][b1]) + rsig[1][a * 8 + c];
+            const double e3 = (dz ? 0.0 : box[2][b2]) + rsig[2][b * 8 + c];
             const double mu = div3((e1 + e2) + e3);
-            mean[a * MA + b * MB + c] = mu;
+            if (INBOX) {  // each class owns its slots of the three boxes
+                box[1][b1] = mu;
+                box[2][b2] = mu;
+            } else {
+                mean[a * MA + b * MB + c] = mu;
+            }
             D0[rbase[0][e >> 3] + (unsigned)(q - (q > j) - (q > l))] = mu;  // row (j,l), column q'
         }
     }
     __syncthreads();
     // views 1 and 2: element (x,y,z) = row (x,y), free index z (contiguous runs in D)
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-        const int e = tid + 256 * h;
+    for (int h = 0; h < TT * TT * TT / NT; h++) {
+        const int e = tid + NT * h;
         const int x = e >> 6, y = (e >> 3) & 7, z = e & 7;
         {   // view 1: row (j, q) = (j0 + x, q0 + y), free l = l0 + z; class (x, z, y)
             const int a = j0 + x, b = q0 + y, f = l0 + z;
             const unsigned base = rbase[1][e >> 3];
             if (base != NOIDX && f < n && f != a && f != b)
-                D1[base + (unsigned)(f - (f > a) - (f > b))] = mean[x * MA + z * MB + y];
+                D1[base + (unsigned)(f - (f > a) - (f > b))] =
+                    INBOX ? box[1][box_pos<BX0>(1, a, f, b, j0, l0, q0, o1)] : mean[x * MA + z * MB + y];
         }
         {   // view 2: row (l, q) = (l0 + x, q0 + y), free j = j0 + z; class (z, x, y)
             const int a = l0 + x, b = q0 + y, f = j0 + z;
             const unsigned base = rbase[2][e >> 3];
             if (base != NOIDX && f < n && f != a && f != b)
-                D2[base + (unsigned)(f - (f > a) - (f > b))] = mean[z * MA + x * MB + y];
+                D2[base + (unsigned)(f - (f > a) - (f > b))] =
+                    INBOX ? box[2][box_pos<BX0>(2, f, a, b, j0, l0, q0, o2)] : mean[z * MA + x * MB + y];
         }
     }
 }
@@ -1773,12 +1785,13 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
     B.ntile_mul = (65536u + (unsigned)A.ntile - 1u) / (unsigned)A.ntile;  // exact y / ntile for y < 64
     dim3 grid(A.ntile, A.ntile * A.ntile, ntri);
     const bool wide = (int64_t)A.g.nblk * A.g.ld2 >= (int64_t(1) << 32);
+    constexpr int NT = 128;  // means in the boxes, 11 CTAs per SM
     if (tma_box0(n) == kBox0) {
-        if (wide) k_transfer_tma<kBox0, true><<<grid, 256, 0, st>>>(B, M);
-        else k_transfer_tma<kBox0, false><<<grid, 256, 0, st>>>(B, M);
+        if (wide) k_transfer_tma<kBox0, true, NT><<<grid, NT, 0, st>>>(B, M);
+        else k_transfer_tma<kBox0, false, NT><<<grid, NT, 0, st>>>(B, M);
     } else {
-        if (wide) k_transfer_tma<kBox0 - 2, true><<<grid, 256, 0, st>>>(B, M);
-        else k_transfer_tma<kBox0 - 2, false><<<grid, 256, 0, st>>>(B, M);
+        if (wide) k_transfer_tma<kBox0 - 2, true, NT><<<grid, NT, 0, st>>>(B, M);
+        else k_transfer_tma<kBox0 - 2, false, NT><<<grid, NT, 0, st>>>(B, M);
     }
     return cudaGetLastError();
 }
