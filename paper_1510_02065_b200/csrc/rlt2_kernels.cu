@@ -363,7 +363,7 @@ __device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int l
 // argmin takes the order key's high word first (the low word only on ties, a warp-uniform
 // branch), then prefers a free column (a lane mask updated once per augmentation), then
 // the lowest column; way[] and the augmenting path (one lane mask) are in lane ids.
-__device__ __noinline__ uint32_t tie_low_word(double minv, uint32_t sg, uint32_t hi, uint32_t mhi)
+__device__ __forceinline__ uint32_t tie_low_word(double minv, uint32_t sg, uint32_t hi, uint32_t mhi)
 {
     const uint32_t lo = static_cast<uint32_t>(__double2loint(minv)) ^ sg;
     const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
