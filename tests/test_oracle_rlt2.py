@@ -297,3 +297,91 @@ def test_stop_rules(orc):
     assert out["status"] in (1, 2) and out["iters"] == 1
     out = orc.bound(inst.F, inst.D, T=3, UB=math.inf)
     assert out["status"] == 0 and out["iters"] == 3
+
+
+# --- the RLT1 ascent's C pair mean ---------------------
+
+RLT1_STEPS = ["spread_b", "transfer_c", "concentrate_c", "concentrate_b"]
+
+
+@pytest.mark.parametrize("family", ["nug", "taib", "uniform"])
+@pytest.mark.parametrize("n", [4, 5, 6])
+def test_rlt1_preservation_every_prefix(orc, family, n):
+    """P:169 for the RLT1 step sequence (Algorithm 1 without the D operations):
+    after every prefix of spread B->C, C pair mean, C->B, B->LB every permutation's cost is
+    unchanged and every entry stays >= 0.  A pair 'mean' with a wrong divisor or a
+    one-sided write breaks the evaluation of the permutations using the pair."""
+    for seed in range(1, 4 if n == 6 else 6):
+        inst = qapgen.make(family, n, seed)
+        st = orc.State(inst.F, inst.D)
+        st.iteration0()
+        for _ in range(3):
+            for name in RLT1_STEPS:
+                getattr(st, name)()
+                check_preservation(st, inst)
+                check_nonneg(st)
+
+
+def test_transfer_c_pairs_equal_and_conserved(orc):
+    """P:222-223 (zero-sum) with reading R13 (mean): after the C transfer each complementary
+    pair c_ij[kl], c_kl[ij] is equal and keeps its sum, on a state where the pairs differ
+    (after spreading B -> C in the RLT1 sequence)."""
+    inst = qapgen.uniform(7, 3)
+    st = orc.State(inst.F, inst.D)
+    st.iteration0()
+    st.spread_b()
+    C0 = st.C.copy()
+    st.transfer_c()
+    C1 = st.C
+    n = st.n
+    differ = 0
+    for i in range(n):
+        for j in range(n):
+            for k in range(i + 1, n):
+                for l in range(n):
+                    if l == j:
+                        continue
+                    a = (i, j, de.skip1(k, i), de.skip1(l, j))
+                    b = (k, l, de.skip1(i, k), de.skip1(j, l))
+                    differ += C0[a] != C0[b]
+                    assert C1[a] == C1[b]
+                    assert abs((C1[a] + C1[b]) - (C0[a] + C0[b])) <= 1e-15 * max(1.0, C0[a] + C0[b])
+    assert differ > 0
+
+
+def test_example_transfer_c(orc):
+    """c_0123 = 4, c_2301 = 2 -> both 3; every other coefficient stays 0."""
+    g = GOLDEN["transfer_c"]
+    n = g["n"]
+    st = _zero_state(orc, n)
+    for i, j, k, l, val in g["c"]:
+        st.C[i, j, de.skip1(k, i), de.skip1(l, j)] = val
+    st.transfer_c()
+    for i, j, k, l, _ in g["c"]:
+        assert st.C[i, j, de.skip1(k, i), de.skip1(l, j)] == g["after"]
+    assert st.C.sum() == 2 * g["after"]
+
+
+@pytest.mark.parametrize("family", ["nug", "taib", "uniform"])
+def test_rlt1_ascent_is_driven_by_the_pair_mean(orc, family):
+    """Why the C transfer is in the RLT1 loop: without it an RLT1 iteration is
+    stationary — spreading b_ij over a residual C_ij whose LAP value is 0 and concentrating
+    it again returns b_ij, and B is a residual with LAP value 0, so LB' = 0 up to rounding.
+    With the pair mean the ascent rises strictly above the Gilmore–Lawler bound (and stays
+    <= the brute-force optimum) on instances where GLB < OPT."""
+    for seed in (1, 2, 3):
+        inst = qapgen.make(family, 7, seed)
+        opt = de.brute_force_opt(inst.F, inst.D)
+        glb = de.gilmore_lawler(inst.F, inst.D)
+        assert glb < opt
+        st = orc.State(inst.F, inst.D)
+        st.iteration0()
+        for _ in range(3):                       # the sequence WITHOUT the pair mean
+            st.spread_b()
+            st.concentrate_c()
+            lbp = st.concentrate_b()
+            assert lbp <= 1e-9 * max(1.0, glb)
+        st = orc.State(inst.F, inst.D)
+        lb = st.rlt1_bound(3)
+        assert lb > glb + 1e-6 * max(1.0, glb), (family, seed, lb, glb)
+        assert lb <= opt * (1 + 1e-12) + 1e-9
