@@ -37,11 +37,12 @@ _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (-O2 -ffp-contract=off, no intrinsics)."""
+    """Compile the oracle with gcc (-O2 -ffp-contract=off, no intrinsics; OpenMP for the
+    optional all-cores mode, 1 thread unless set_threads() raises it)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-                               "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+                               "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -89,8 +90,20 @@ def lib():
         L.oracle_rlt1_bound.argtypes = [ct.c_void_p, ct.c_int, ct.POINTER(ct.c_double)]
         L.oracle_strong_branch.argtypes = [ct.c_int, _i64p, _i64p, ct.c_int, _i32p, _i32p, ct.c_int, _f64p,
                                            ct.POINTER(ct.c_int), ct.POINTER(ct.c_int)]
+        L.oracle_set_threads.argtypes = [ct.c_int]
+        L.oracle_qap_bruteforce.argtypes = [ct.c_int, _i64p, _i64p, ct.POINTER(ct.c_int64), _i32p]
         _lib = L
     return _lib
+
+
+def set_threads(t: int) -> None:
+    """Host threads for the independent units of each step (1 = the plain sequential oracle;
+    every thread count gives bit-identical results)."""
+    lib().oracle_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
 
 
 class OracleError(RuntimeError):
@@ -274,6 +287,18 @@ def bnb(F, Dist, T: int = 3, K: float = 0.0, UB0: float = math.inf, sb_iters: in
     _check(lib().oracle_bnb(N, F, Dist, T, K, UB0, sb_iters, int(warm), ct.byref(best), perm, ct.byref(b), ct.byref(l),
                             ct.byref(p), ct.byref(c)), "bnb")
     return dict(opt=best.value, perm=perm, bounded=b.value, leaves=l.value, pruned=p.value, sb_cut=c.value)
+
+
+def qap_bruteforce(F, Dist):
+    """Brute-force QAP optimum over all N! permutations (test pin; N <= 13): (opt, first
+    permutation in lexicographic order reaching it)."""
+    F = np.ascontiguousarray(F, dtype=np.int64)
+    Dist = np.ascontiguousarray(Dist, dtype=np.int64)
+    N = F.shape[0]
+    best = ct.c_int64()
+    perm = np.zeros(N, np.int32)
+    _check(lib().oracle_qap_bruteforce(N, F, Dist, ct.byref(best), perm), "qap_bruteforce")
+    return best.value, perm
 
 
 def strong_branch(F, Dist, fixed=(), T: int = 1):

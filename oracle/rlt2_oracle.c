@@ -42,6 +42,14 @@
 #define ORC_E_NUMERIC 5
 #define ORC_E_STATE 6
 
+/* Host threads for the loops over independent units (blocks, classes, pairs (i,j)): 1 by
+ * default (the tests); bench.py's all-cores baseline raises it.  Every unit writes only its
+ * own entries and runs its operations in the fixed order below, so the result is
+ * bit-identical for every thread count (SURVEY.md §8(d) oracle timing mode (ii)).        */
+static int g_threads = 1;
+void oracle_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
+int oracle_get_threads(void) { return g_threads; }
+
 /* ------------------------------------------------------------------------- */
 /* O2 — one linear assignment problem.                           */
 /* ------------------------------------------------------------------------- */
@@ -161,6 +169,44 @@ int oracle_lap_bruteforce(int m, const double *M, double *best_out, int32_t *ass
     bf_rec(m, M, 0, perm, taken, 0.0, &best, bp);
     *best_out = best;
     if (assign) memcpy(assign, bp, (size_t)m * sizeof(int32_t));
+    return ORC_OK;
+}
+
+/* Brute-force QAP optimum (test pin, not the method): enumerate all N! permutations in
+ * lexicographic order and evaluate the Koopmans–Beckmann objective of P:84,
+ * sum_{i,k} f_ik d_{pi(i) pi(k)}, accumulated facility by facility (the terms of facility d
+ * with the facilities 0..d fixed before it).  Returns the minimum and the first
+ * permutation reaching it.  N <= 13 (13! = 6.2e9 leaves).                            */
+typedef struct { int N; const int64_t *F, *Dist; int32_t perm[16]; char used[16];
+                 int64_t best; int32_t best_perm[16]; } bfq_ctx;
+
+static void bfq_rec(bfq_ctx *c, int d, int64_t partial)
+{
+    if (d == c->N) {
+        if (partial < c->best) { c->best = partial; memcpy(c->best_perm, c->perm, sizeof c->perm); }
+        return;
+    }
+    const int N = c->N;
+    for (int x = 0; x < N; x++) {
+        if (c->used[x]) continue;
+        int64_t add = c->F[d * N + d] * c->Dist[x * N + x];
+        for (int t = 0; t < d; t++)
+            add += c->F[d * N + t] * c->Dist[x * N + c->perm[t]] + c->F[t * N + d] * c->Dist[c->perm[t] * N + x];
+        c->used[x] = 1; c->perm[d] = x;
+        bfq_rec(c, d + 1, partial + add);
+        c->used[x] = 0;
+    }
+}
+
+int oracle_qap_bruteforce(int N, const int64_t *F, const int64_t *Dist, int64_t *best_out, int32_t *perm_out)
+{
+    if (N < 1 || N > 13) return ORC_E_ARG;
+    bfq_ctx c;
+    memset(&c, 0, sizeof c);
+    c.N = N; c.F = F; c.Dist = Dist; c.best = INT64_MAX;
+    bfq_rec(&c, 0, 0);
+    *best_out = c.best;
+    memcpy(perm_out, c.best_perm, sizeof(int32_t) * N);
     return ORC_OK;
 }
 
@@ -381,16 +427,20 @@ ostate *oracle_state_fold(const ostate *s, int a, int b, int *err)
  * row-major order, LAP on C_ij (size n-1), C_ij <- residual, b_ij += S.          */
 int oracle_concentrate_c(ostate *s)
 {
-    int n = s->n, m = n - 1;
+    int n = s->n, m = n - 1, err = ORC_OK;
+#pragma omp parallel for collapse(2) schedule(dynamic) num_threads(g_threads)
     for (int i = 0; i < n; i++)
         for (int j = 0; j < n; j++) {
             double *blk = s->C + (size_t)(i * n + j) * m * m;
             double S;
             int st = oracle_lap(m, blk, blk, NULL, NULL, NULL, &S, NULL);
-            if (st) return st;
+            if (st) {
+#pragma omp atomic write
+                err = st;
+            }
             s->B[i * n + j] = s->B[i * n + j] + S;
         }
-    return ORC_OK;
+    return err;
 }
 
 /* Cost concentration B -> LB ("LB' <- Concentrate(B)", "LB <- LB + LB'"). */
@@ -420,6 +470,7 @@ int oracle_iteration0(ostate *s)
 int oracle_spread_b(ostate *s)
 {
     int n = s->n, m = n - 1;
+#pragma omp parallel for collapse(2) schedule(static) num_threads(g_threads)
     for (int i = 0; i < n; i++)
         for (int j = 0; j < n; j++) {
             double beta = s->B[i * n + j] / (double)(n - 1);
@@ -443,6 +494,7 @@ int oracle_spread_c_transfer_d(ostate *s)
 {
     int n = s->n;
     double *sigma = malloc(sizeof(double) * (size_t)s->nblk);
+#pragma omp parallel for collapse(2) schedule(static) num_threads(g_threads)
     for (int i = 0; i < n; i++)
         for (int j = 0; j < n; j++)
             for (int k = i + 1; k < n; k++)
@@ -451,10 +503,13 @@ int oracle_spread_c_transfer_d(ostate *s)
                     int32_t b = s->blk[((size_t)(i * n + j) * n + k) * n + l];
                     sigma[b] = (s->C[cidx(s, i, j, k, l)] + s->C[cidx(s, k, l, i, j)]) / (double)(2 * (n - 2));
                 }
+    /* every stored entry belongs to exactly one class: the classes are independent, and
+       the loop order (here (i, j) outermost for the threads) changes no bit */
+#pragma omp parallel for collapse(2) schedule(dynamic) num_threads(g_threads)
     for (int i = 0; i < n; i++)
-        for (int k = i + 1; k < n; k++)
-            for (int p = k + 1; p < n; p++)
-                for (int j = 0; j < n; j++)
+        for (int j = 0; j < n; j++)
+            for (int k = i + 1; k < n; k++)
+                for (int p = k + 1; p < n; p++)
                     for (int l = 0; l < n; l++) {
                         if (l == j) continue;
                         for (int q = 0; q < n; q++) {
@@ -479,7 +534,9 @@ int oracle_spread_c_transfer_d(ostate *s)
  * coefficients c_ij[kl] and c_kl[ij] (reading R12).                              */
 int oracle_concentrate_d(ostate *s)
 {
-    int n = s->n, m = n - 2;
+    int n = s->n, m = n - 2, err = ORC_OK;
+    /* each block credits only its own two coefficients: blocks are independent */
+#pragma omp parallel for collapse(2) schedule(dynamic) num_threads(g_threads)
     for (int i = 0; i < n; i++)
         for (int j = 0; j < n; j++)
             for (int k = i + 1; k < n; k++)
@@ -489,11 +546,14 @@ int oracle_concentrate_d(ostate *s)
                     double *blk = s->D + (size_t)b * m * m;
                     double S;
                     int st = oracle_lap(m, blk, blk, NULL, NULL, NULL, &S, NULL);
-                    if (st) return st;
+                    if (st) {
+#pragma omp atomic write
+                        err = st;
+                    }
                     s->C[cidx(s, i, j, k, l)] = s->C[cidx(s, i, j, k, l)] + S;
                     s->C[cidx(s, k, l, i, j)] = s->C[cidx(s, k, l, i, j)] + S;
                 }
-    return ORC_OK;
+    return err;
 }
 
 /* Transfer between complementary costs of C (reading R13: pair mean).  */

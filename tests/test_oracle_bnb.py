@@ -104,3 +104,36 @@ def test_bnb_strong_branching_optimum(orc, family, n):
     assert out["opt"] == opt and inst.evaluate(out["perm"]) == opt
     plain = orc.bnb(inst.F, inst.D, T=2)
     assert plain["opt"] == opt
+
+
+# --- BASELINE config 2 (nug12-shaped, seed 1): oracle B&B vs brute force -------------------
+
+def _golden_n12():
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden", "n12_nug_seed1_bnb.json")))
+
+
+@pytest.mark.parametrize("family", ["nug", "taib", "uniform"])
+def test_qap_bruteforce_matches_enumeration(orc, family):
+    """The C enumerator behind the N = 12 golden optimum agrees with the vectorised numpy
+    enumeration (tests/dualeval.py) and its permutation attains the optimum."""
+    for n in (5, 7, 8):
+        inst = qapgen.make(family, n, 3)
+        opt, perm = orc.qap_bruteforce(inst.F, inst.D)
+        assert opt == de.brute_force_opt(inst.F, inst.D)
+        assert inst.evaluate([int(x) for x in perm]) == opt
+
+
+def test_bnb_config2_n12_optimum_is_bruteforce(orc):
+    """BASELINE config 2: the oracle B&B with T = 10 (cold children) solves the nug12-shaped
+    instance to the brute-force optimum over all 12! permutations (committed by
+    scripts/golden_bnb_n12.py), with the committed node counts."""
+    g = _golden_n12()
+    inst = qapgen.nug(g["N"], 1)
+    o = orc.bnb(inst.F, inst.D, T=g["T"])
+    assert o["opt"] == g["bruteforce"]["opt"]
+    assert inst.evaluate([int(x) for x in o["perm"]]) == g["bruteforce"]["opt"]
+    c = g["bnb"]["cold"]
+    assert (o["bounded"], o["leaves"], o["pruned"]) == (c["bounded"], c["leaves"], c["pruned"])
+    assert list(o["perm"]) == c["perm"]

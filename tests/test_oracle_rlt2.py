@@ -385,3 +385,20 @@ def test_rlt1_ascent_is_driven_by_the_pair_mean(orc, family):
         lb = st.rlt1_bound(3)
         assert lb > glb + 1e-6 * max(1.0, glb), (family, seed, lb, glb)
         assert lb <= opt * (1 + 1e-12) + 1e-9
+
+
+def test_all_cores_mode_is_bit_identical(orc):
+    """SURVEY §8(d) oracle timing mode (ii): the OpenMP loops over independent units (blocks,
+    classes, pairs) give the same bits as the sequential oracle."""
+    inst = qapgen.taib(12, 2)
+    ref = orc.State(inst.F, inst.D)
+    r1 = ref.bound(3, trace=True)
+    try:
+        orc.set_threads(4)
+        st = orc.State(inst.F, inst.D)
+        r4 = st.bound(3, trace=True)
+    finally:
+        orc.set_threads(1)
+    assert (r1["trace"] == r4["trace"]).all() and r1["lb"] == r4["lb"]
+    for a, b in ((ref.B, st.B), (ref.C, st.C), (ref.D, st.D)):
+        assert a.tobytes() == b.tobytes()
