@@ -192,8 +192,6 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lap-warps", type=int, default=0)
     ap.add_argument("--no-bnb", action="store_true")
-    ap.add_argument("--fused", action="store_true", help="QAP_FLAG_FUSED: transfer + level-2 LAPs in one kernel")
-    ap.add_argument("--class-layout", action="store_true", help="QAP_FLAG_CLASS_LAYOUT (A/B of the level-2 layouts)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of one sharded bound")
     args = ap.parse_args()
 
@@ -216,12 +214,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     n, T = args.n, T_ITERS
     inst = qapgen.nug(n, SEED)
-    FL = (pkg.QAP_FLAG_TIME_KERNELS | (pkg.QAP_FLAG_FUSED if args.fused else 0)
-          | (pkg.QAP_FLAG_CLASS_LAYOUT if args.class_layout or args.fused else 0))
+    FL = pkg.QAP_FLAG_TIME_KERNELS
     stream = torch.cuda.current_stream()
-    sharded, shard_err = False, None
+    sharded = False
     if world > 1 and not args.replicas:
-        # one bound sharded over all ranks: NCCL id from rank 0
+        # one bound sharded over all ranks: NCCL id from rank 0.  A failure on
+        # any rank ends the run with an error (never a silent switch to replicas: --replicas
+        # asks for those explicitly).
+        err = None
         try:
             uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
             if rank == 0:
@@ -231,19 +231,20 @@ def main():
                                     flags=FL, lap_warps=args.lap_warps,
                                     world=world, rank=rank, nccl_id=bytes(uid.cpu().numpy()))
             sharded = True
-        except Exception as ex:  # reported in the JSON line; replicas below
-            shard_err = f"{type(ex).__name__}: {ex}"
-    if not sharded:
-        h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
-                                flags=FL, lap_warps=args.lap_warps)
-    if dist:
+        except Exception as ex:
+            err = f"{type(ex).__name__}: {ex}"
         ok = torch.tensor([1 if sharded else 0], device="cuda")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if sharded and ok.item() == 0:  # some rank failed: everybody falls back to replicas
-            pkg.qap_destroy(h)
-            sharded = False
-            h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
-                                    flags=FL, lap_warps=args.lap_warps)
+        if ok.item() == 0:
+            print(json.dumps({"error": "sharded handle creation failed" + (f" on rank {rank}: {err}" if err else
+                                                                              " on another rank"),
+                              "hint": "--replicas runs one independent bound per GPU instead"}),
+                  file=sys.stderr, flush=True)
+            dist.destroy_process_group()
+            return 1
+    else:
+        h = pkg.qap_rlt2_create(n, inst.F, inst.D, device=local_rank, stream=stream.cuda_stream,
+                                flags=FL, lap_warps=args.lap_warps)
 
     def step(hh):
         pkg.qap_rlt2_fix(hh, ())
@@ -404,12 +405,8 @@ def main():
         alg_bytes = 16 * shard_entries
     dom = max(("lap2", "transfer"), key=lambda k: per.get(k, {}).get("share", 0))
     achieved = alg_bytes / (per[dom]["avg_ms"] / 1e3) / 1e9
-    xl = (not sharded) and n >= 16 and (args.class_layout or args.fused)  # class layout
-    fused = xl and args.fused and "transfer" not in per
-    names = {"lap2": "k_fused_x (transfer + level-2 concentration in one persistent kernel, class layout)" if fused
-             else "k_lap<1,1,0,1> (level-2 concentration, class layout, TMA gather4/scatter4)" if xl
-             else "k_lap<1> (level-2 concentration)",
-             "transfer": "k_transfer_x (class layout, TMA boxes)" if xl else "k_transfer"}
+    names = {"lap2": "k_lap<1> (level-2 concentration)" if n - 2 <= 32 else "k_lap<2> (level-2 concentration)",
+             "transfer": "k_transfer_tma" if n >= 10 and not sharded else "k_transfer"}
     roof = {"bound": "hbm", "kernel": names[dom],
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": profiled_traffic(dom), "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
@@ -429,11 +426,6 @@ def main():
         a2 = alg_bytes / (per[other]["avg_ms"] / 1e3) / 1e9
         roof["other_kernel"] = {"kernel": names[other], "achieved": a2, "frac": a2 / peak,
                                 "traffic": profiled_traffic(other)}
-    if fused:  # one launch moves every stored entry twice (transfer, then LAP): 32 B / entry
-        roof["alg_bytes_per_launch"] = 2 * alg_bytes
-        roof["achieved"] = 2 * achieved
-        roof["frac"] = 2 * achieved / peak
-        roof["note"] = "fused launch: transfer (16 B/entry) + level-2 LAPs (16 B/entry)"
     iter_ms = (per["sigma"]["avg_ms"] + per.get("transfer", {"avg_ms": 0.0})["avg_ms"] + per["lap2"]["avg_ms"]
                + per["lap1"]["avg_ms"] * T / (T + 1) + per["lap0"]["avg_ms"])
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -441,8 +433,8 @@ def main():
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_cfg(n, {"parallelism": (f"one bound sharded over {world} GPUs (first-facility LPT "
                                                        "partition, NCCL exchange + all-gather)") if sharded else
-                                       ("replicas (one independent bound per GPU)" + (f"; sharding failed: {shard_err}"
-                                        if shard_err else "")) if world > 1 else "1 GPU"}),
+                                       "replicas (--replicas: one independent bound per GPU)" if world > 1
+                                       else "1 GPU"}),
             "laps_per_s": value * laps_per_iter(n),
             "value_with_kernel_events": {"value": iters_total / (ms_ev / 1e3), "unit": "iters/s",
                                          "note": "same steps with a CUDA-event pair around every launch "

@@ -52,6 +52,27 @@ typedef enum {
     QAP_E_STATE = 6      /* call not valid in the handle's current state                         */
 } qap_status;
 
+/*
+ * Host-staged collectives of a sharded bound, an alternative to NCCL: the
+ * library copies its exchange buffers to pinned host memory, calls these callbacks (same
+ * order on every rank, from the thread that called the library), and copies the results
+ * back.  For processes that share one GPU (NCCL refuses two ranks on one device) and for
+ * testing the sharded data path over any host transport (e.g. torch.distributed gloo).
+ *   exchange: for every peer q != rank with count[q] > 0, send send[off[q] .. off[q] +
+ *             count[q]) to q and receive q's range into recv[off[q] .. off[q] + count[q])
+ *             (counts and offsets in doubles; both ranks of a pair use the same range size).
+ *   allgather: S_all[lo[q] .. lo[q+1]) holds rank q's values on rank q; afterwards every
+ *             rank holds all of them (lo has world + 1 entries).
+ * Return 0 on success; anything else fails the bound with QAP_E_NCCL.  The pointers are
+ * valid only during the call.
+ */
+typedef struct {
+    void *ctx;
+    int32_t (*exchange)(void *ctx, const double *send, double *recv, const int64_t *off, const int64_t *count,
+                        int32_t world, int32_t rank);
+    int32_t (*allgather)(void *ctx, double *S_all, const int64_t *lo, int32_t world, int32_t rank);
+} qap_host_transport;
+
 typedef struct {
     int32_t device;       /* CUDA device ordinal; -1 = current device                         */
     void *cuda_stream;    /* cudaStream_t to enqueue on; NULL = legacy default stream          */
@@ -61,22 +82,14 @@ typedef struct {
     int32_t rank;         /* this process's rank in [0, world)                                 */
     const void *nccl_id;  /* world > 1: 128-byte ncclUniqueId from qap_nccl_unique_id on rank
                              0, broadcast by the caller; every rank then calls create (collective) */
+    const qap_host_transport *host_transport;  /* world > 1 and non-NULL: host-staged collectives
+                             through these callbacks instead of NCCL (nccl_id unused); copied */
 } qap_rlt2_opts;
 
 #define QAP_FLAG_TIME_KERNELS 1   /* record CUDA events around every launch (qap_rlt2_kernel_stats) */
-#define QAP_FLAG_OVERLAP 2        /* run the D transfer and the level-2 LAPs concurrently on two
-                                     internal streams (experimental; default: one after the other) */
 #define QAP_FLAG_NO_GRAPH 4       /* do not replay the iteration loop from a cached CUDA graph     */
 #define QAP_FLAG_LDG_TRANSFER 8   /* transfer with per-element loads instead of tensor-map TMA    */
-#define QAP_FLAG_CLASS_LAYOUT 16  /* bound nodes with n >= 16 in the class layout of DESIGN.md §6
-                                     (per-member arrays: the transfer moves dense TMA boxes, the
-                                     level-2 LAP gathers its rows with TMA gather4/scatter4);
-                                     bit-identical results; default: the stored-block layout.
-                                     qap_rlt2_dual_copy always exports the block layout          */
-#define QAP_FLAG_FUSED 32         /* with QAP_FLAG_CLASS_LAYOUT, 16 <= n <= 34: each iteration's
-                                     transfer and level-2 LAPs as ONE persistent kernel (warps take
-                                     transfer tiles or LAPs whose facility is transferred);
-                                     experimental, bit-identical, measured slower */
+/* other bits are reserved: qap_rlt2_create returns QAP_E_ARG for them                    */
 
 typedef struct {
     double lb;          /* kappa + dual bound after the last iteration run            */

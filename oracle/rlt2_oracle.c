@@ -55,11 +55,12 @@ int oracle_get_threads(void) { return g_threads; }
 /* ------------------------------------------------------------------------- */
 /*
  * Shortest-augmenting-path form of the Hungarian algorithm (P:205 cites Munkres;
- * reading R4: an exact Hungarian-type solver).  Written as the classic O(m^3)
- * potentials form: rows are inserted one at a time in ascending order, each by a
- * Dijkstra search over reduced costs; column 0 is a dummy holding the row being
- * inserted.  Cold start u = v = 0, which yields the canonical dual of reading R5
- * (v componentwise maximal subject to v <= 0).
+ * reading R4: an exact Hungarian-type solver).  Munkres' row reduction first (u = row
+ * minima, v = 0, rows matched greedily to the lowest column of their minimum), then the
+ * classic O(m^3) potentials form for the rows left: each is inserted, in ascending
+ * order, by a Dijkstra search over reduced costs; column 0 is a dummy holding the row
+ * being inserted.  v starts at 0 and only Dijkstra distances are taken off it, which
+ * yields the canonical dual of reading R5 (v componentwise maximal subject to v <= 0).
  *
  * Tie rule (reading R6): the next column settled is the unused column minimising
  * the key (minv[j], column already matched?, j) lexicographically — smallest
@@ -86,7 +87,24 @@ int oracle_lap(int m, const double *M, double *R, int32_t *assign, double *u_out
     char *used = malloc((size_t)m + 1);
     int64_t steps = 0;
 
+    /* Munkres' first step (P:205 cites the Hungarian method of Munkres; reading R4): every
+     * row is reduced by its minimum, u[r] = min_s M[r][s], v = 0.  Initial partial
+     * assignment on the zeros this creates: for r ascending, row r takes the lowest column
+     * attaining its minimum unless an earlier row took that column.  The dual stays
+     * feasible and v = 0 is untouched, so the final dual is still the canonical one of
+     * reading R5 (pinned by Bellman–Ford in tests/test_oracle_lap.py).                   */
+    char *rmatched = calloc((size_t)m + 1, 1);
+    for (int r = 1; r <= m; r++) {
+        int a = 1;
+        for (int j = 2; j <= m; j++)
+            if (M[(size_t)(r - 1) * m + (j - 1)] < M[(size_t)(r - 1) * m + (a - 1)]) a = j;
+        u[r] = M[(size_t)(r - 1) * m + (a - 1)];
+        if (p[a] == 0) { p[a] = r; rmatched[r] = 1; }
+    }
+
+    /* the remaining rows, ascending, each by one shortest-augmenting-path search */
     for (int i = 1; i <= m; i++) {
+        if (rmatched[i]) continue;
         p[0] = i;
         int j0 = 0;
         for (int j = 0; j <= m; j++) { minv[j] = INFINITY; used[j] = 0; }
@@ -140,7 +158,7 @@ int oracle_lap(int m, const double *M, double *R, int32_t *assign, double *u_out
     if (v_out) for (int s = 0; s < m; s++) v_out[s] = v[s + 1];
     if (S_out) *S_out = S;
     if (steps_out) *steps_out = steps;
-    free(u); free(v); free(minv); free(p); free(way); free(used); free(a);
+    free(u); free(v); free(minv); free(p); free(way); free(used); free(a); free(rmatched);
     return st;
 }
 

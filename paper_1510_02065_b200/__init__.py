@@ -24,11 +24,8 @@ LIB_PATH = os.path.join(HERE, "libqaprlt2.so")
 QAP_OK, QAP_E_ARG, QAP_E_CAPACITY, QAP_E_CUDA, QAP_E_NCCL, QAP_E_NUMERIC, QAP_E_STATE = range(7)
 STATUS_NAMES = ["OK", "E_ARG", "E_CAPACITY", "E_CUDA", "E_NCCL", "E_NUMERIC", "E_STATE"]
 QAP_FLAG_TIME_KERNELS = 1
-QAP_FLAG_OVERLAP = 2
 QAP_FLAG_NO_GRAPH = 4
 QAP_FLAG_LDG_TRANSFER = 8
-QAP_FLAG_CLASS_LAYOUT = 16
-QAP_FLAG_FUSED = 32
 PHASE_ITER0, PHASE_TRANSFER, PHASE_CONC_D, PHASE_CONC_C, PHASE_CONC_B = range(5)
 KERNEL_KINDS = ["init", "sigma", "transfer", "lap2", "lap1", "lap0"]
 

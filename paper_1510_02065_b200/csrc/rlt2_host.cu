@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -45,8 +48,7 @@ struct qap_rlt2 {
     double *dB = nullptr, *dC = nullptr, *dD = nullptr, *dSigma = nullptr, *dTrace = nullptr;
     int *dTriples = nullptr;
     Sched *dSched = nullptr;
-    cudaStream_t sL = nullptr, sT = nullptr;  // LAP (high priority) / transfer (low priority)
-    cudaEvent_t evJoin = nullptr, evS = nullptr, evL = nullptr;
+    cudaEvent_t evJoin = nullptr;  // orders this handle's stream against another's (fold, copy)
     Ctl *dCtl = nullptr;
     int trace_cap = 4096;
     Node node{};
@@ -89,17 +91,6 @@ struct qap_rlt2 {
     // tensor maps of D for k_transfer_tma, encoded for node size tma_n (0: none / failed)
     TmaMaps tma{};
     int tma_n = 0;
-    // class layout X of the level-2 dual (QAP_FLAG_CLASS_LAYOUT): allocated for
-    // n_cap >= kXMin on single-rank handles; the block buffer dD is then allocated on first
-    // need (bytesD).
-    // dvalid: bit 0 = dD holds the current D, bit 1 = dX does (both while D is lazily zero).
-    double *dX = nullptr;
-    size_t bytesD = 0;
-    int dvalid = 3;
-    CUtensorMap xmap{};   // 4-D [np][n][n][3 ntri], 8x8x8x1 boxes (k_transfer_x)
-    CUtensorMap xrow{};   // 2-D [3 ntri n n][np], {np, 1} boxes (level-2 LAP gather4/scatter4)
-    CUtensorMap xa{}, xb{};  // 4-D as xmap with {8,8,4,1} / {4,8,8,1} boxes (k_fused_x tiles)
-    int xmap_n = 0;
 };
 
 static std::string g_create_error;
@@ -169,17 +160,12 @@ static void free_all(qap_rlt2 *h)
     cudaFree(h->dB);
     cudaFree(h->dC);
     cudaFree(h->dD);
-    cudaFree(h->dX);
     cudaFree(h->dSigma);
     cudaFree(h->dTrace);
     cudaFree(h->dCtl);
     cudaFree(h->dTriples);
     cudaFree(h->dSched);
-    if (h->sL) cudaStreamDestroy(h->sL);
-    if (h->sT) cudaStreamDestroy(h->sT);
     if (h->evJoin) cudaEventDestroy(h->evJoin);
-    if (h->evS) cudaEventDestroy(h->evS);
-    if (h->evL) cudaEventDestroy(h->evL);
     cudaFree(h->dRc);
     cudaFree(h->dRb);
     cudaFree(h->dRlbd);
@@ -217,8 +203,6 @@ static qap_status check_instance(qap_rlt2 *h, int N, const int64_t *F, const int
 }
 
 extern "C" {
-static qap_status d_layout(qap_rlt2 *h, int want);
-static qap_status ensure_dD(qap_rlt2 *h);
 
 static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, const qap_rlt2_opts *opts,
                               qap_rlt2 **out, bool loopback, int n_cap = 0);
@@ -245,8 +229,13 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
     const int rank = world > 1 ? opts->rank : 0;
     if (world > 1) {
         if (rank < 0 || rank >= world || world > 64) return fail(nullptr, QAP_E_ARG, "bad rank / world");
-        if (!loopback && !opts->nccl_id) return fail(nullptr, QAP_E_ARG, "world > 1 needs opts->nccl_id");
+        if (!loopback && !opts->nccl_id && !opts->host_transport)
+            return fail(nullptr, QAP_E_ARG, "world > 1 needs opts->nccl_id or opts->host_transport");
+        if (!loopback && opts->host_transport && (!opts->host_transport->exchange || !opts->host_transport->allgather))
+            return fail(nullptr, QAP_E_ARG, "host_transport needs both callbacks");
     }
+    if (opts && (opts->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_NO_GRAPH | QAP_FLAG_LDG_TRANSFER)))
+        return fail(nullptr, QAP_E_ARG, "unknown flag bits");
     qap_rlt2 *h = new qap_rlt2();
     h->N = N;
     h->world = world;
@@ -295,12 +284,7 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         delete h;
         return s;
     }
-    // class layout when asked for and compatible with the other flags
-    const bool xl = world == 1 && !loopback && h->n_cap >= kXMin && (h->flags & QAP_FLAG_CLASS_LAYOUT) &&
-                    !(h->flags & (QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER));
-    const size_t bytesX = xl ? x_doubles(h->n_cap) * 8 : 0;
-    h->bytesD = bytesD;
-    const size_t need = (xl ? bytesX : bytesD) + bytesC + bytesB + bytesS + (64u << 20);
+    const size_t need = bytesD + bytesC + bytesB + bytesS + (64u << 20);
     if (need > freeb) {
         delete h;
         char msg[160];
@@ -318,11 +302,7 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
     ALLOC(h->dDist, (size_t)N * N * 8);
     ALLOC(h->dB, bytesB);
     ALLOC(h->dC, bytesC);
-    if (xl) {
-        ALLOC(h->dX, bytesX);
-    } else {
-        ALLOC(h->dD, bytesD);
-    }
+    ALLOC(h->dD, bytesD);
     ALLOC(h->dSigma, bytesS);
     ALLOC(h->dTrace, (size_t)h->trace_cap * 8);
     ALLOC(h->dCtl, sizeof(Ctl));
@@ -334,7 +314,9 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         ALLOC(h->dSend, h->slots_cap * kSlot * 8 + 16);
         ALLOC(h->dRecv, h->slots_cap * kSlot * 8 + 16);
         ALLOC(h->dSall, (size_t)gN.nblk * 8 + 16);
-        if (!loopback) {
+        if (!loopback && opts->host_transport) {
+            h->tp = make_host_transport(*opts->host_transport, world, rank);
+        } else if (!loopback) {
             const char *why = "";
             h->tp = make_nccl_transport(opts->nccl_id, world, rank, h->device, &why);
             if (!h->tp) {
@@ -346,13 +328,7 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         }
     }
     {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if ((e = cudaStreamCreateWithPriority(&h->sL, cudaStreamNonBlocking, hi)) != cudaSuccess ||
-            (e = cudaStreamCreateWithPriority(&h->sT, cudaStreamNonBlocking, lo)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&h->evS, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&h->evL, cudaEventDisableTiming)) != cudaSuccess ||
+        if ((e = cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaStreamCreateWithFlags(&h->sCap, cudaStreamNonBlocking)) != cudaSuccess) {
             free_all(h);
             delete h;
@@ -455,7 +431,6 @@ qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_
     if (e != cudaSuccess) return cuda_fail(h, e, "k_init");
     h->next_phase = PH_FRESH;
     h->d_zero = 1;
-    h->dvalid = 3;
     h->b_zero = 0;
     h->c_zero = 0;
     return QAP_OK;
@@ -492,10 +467,6 @@ qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, i
     }
     cudaError_t e = cudaSetDevice(child->device);
     if (e != cudaSuccess) return cuda_fail(child, e, "device");
-    qap_rlt2 *par = const_cast<qap_rlt2 *>(parent);
-    qap_status ls = d_layout(par, 1);  // the fold reads the parent's stored blocks
-    if (ls != QAP_OK) return fail(child, ls, "parent layout: " + par->err);
-    if ((ls = ensure_dD(child)) != QAP_OK) return ls;
     // order: parent's pending work -> fold (child stream) -> later parent work
     if ((e = cudaEventRecord(parent->evJoin, parent->stream)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(child->stream, parent->evJoin, 0)) != cudaSuccess)
@@ -525,18 +496,12 @@ qap_status qap_rlt2_fold(qap_rlt2 *child, const qap_rlt2 *parent, int32_t fac, i
         return cuda_fail(child, e, "fold ordering");
     child->next_phase = PH_FRESH;
     child->d_zero = parent->d_zero;
-    child->dvalid = parent->d_zero ? 3 : 1;
     child->b_zero = 0;
     child->c_zero = 0;
     return QAP_OK;
 }
 
-// Enqueue one phase of Algorithm 1.  `st` is the stream the call's work is ordered on.
-// In overlapped mode the TRANSFER phase runs on the low-priority stream sT and the level-2
-// LAP kernel (CONC_D) on the high-priority stream sL concurrently with it: LAP warps take
-// blocks in facility order and wait for the transfer of their facility on the device
-// (Sched counters).  Both join back into `st`.
-static TransferArgs transfer_args(qap_rlt2 *h, int publish)
+static TransferArgs transfer_args(qap_rlt2 *h)
 {
     TransferArgs A{};
     A.g = h->geom;
@@ -547,7 +512,6 @@ static TransferArgs transfer_args(qap_rlt2 *h, int publish)
     A.ctl = h->dCtl;
     A.sched = h->dSched;
     A.ntile = (h->geom.n + TT - 1) / TT;
-    A.publish = publish;
     if (h->world > 1) {
         A.tiles = h->dTiles;
         A.tinfo = h->dTinfo;
@@ -571,11 +535,11 @@ static cudaError_t run_shard_sub(qap_rlt2 *h, int phase, int sub, cudaStream_t s
             return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->dSched, s);
         });
         if (e) return e;
-        TransferArgs A = transfer_args(h, 0);
+        TransferArgs A = transfer_args(h);
         A.pack = 1;
         e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, (int)P.tiles.size(), s); });
     } else if (phase == QAP_PHASE_TRANSFER && sub == 1) {
-        TransferArgs A = transfer_args(h, 0);
+        TransferArgs A = transfer_args(h);
         e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, (int)P.tiles.size(), s); });
         h->d_zero = 0;
         h->b_zero = h->c_zero = 1;
@@ -635,87 +599,7 @@ static bool tma_maps(qap_rlt2 *h)
     return ok;
 }
 
-// ---- layouts of the level-2 dual ----------------------------------------
-// 4-D tensor map of the class layout X for node size n: [np][n][n][3 ntri], 8x8x8x1 boxes
-static bool x_map(qap_rlt2 *h)
-{
-    const Geom &g = h->geom;
-    if (!h->dX) return false;
-    if (h->xmap_n == g.n) return true;
-    if (h->xmap_n == -g.n) return false;
-    auto enc = tma_encoder();
-    bool ok = enc != nullptr && g.n >= TT;
-    if (ok) {
-        const cuuint64_t np = (cuuint64_t)g.np, n = (cuuint64_t)g.n;
-        cuuint64_t dims[4] = {np, n, n, 3 * (cuuint64_t)g.ntri};
-        cuuint64_t strides[3] = {np * 8, n * np * 8, n * n * np * 8};
-        cuuint32_t box[4] = {(cuuint32_t)TT, (cuuint32_t)TT, (cuuint32_t)TT, 1u};
-        cuuint32_t es[4] = {1, 1, 1, 1};
-        ok = enc(&h->xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dX, dims, strides, box, es,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-        cuuint64_t dims2[2] = {np, 3 * (cuuint64_t)g.ntri * n * n};
-        cuuint64_t strides2[1] = {np * 8};
-        // box width = the LAP's cost-buffer row stride (>= n + 2, multiple of 4): the columns
-        // beyond np are zero-filled on load and clipped on store
-        cuuint32_t box2[2] = {(cuuint32_t)((g.n + 5) & ~3), 1u};
-        ok = ok && enc(&h->xrow, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, h->dX, dims2, strides2, box2, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-        cuuint32_t boxa[4] = {8u, 8u, 4u, 1u}, boxb[4] = {4u, 8u, 8u, 1u};
-        ok = ok && enc(&h->xa, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dX, dims, strides, boxa, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-        ok = ok && enc(&h->xb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, h->dX, dims, strides, boxb, es,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-    }
-    h->xmap_n = ok ? g.n : -g.n;
-    return ok;
-}
-// the current node is bounded in the class layout
-static bool use_x(qap_rlt2 *h)
-{
-    return h->dX && h->world == 1 && !h->loopback && h->geom.n >= kXMin &&
-           (h->flags & QAP_FLAG_CLASS_LAYOUT) && !(h->flags & (QAP_FLAG_OVERLAP | QAP_FLAG_LDG_TRANSFER)) &&
-           x_map(h);
-}
-static qap_status ensure_dD(qap_rlt2 *h)
-{
-    if (h->dD) return QAP_OK;
-    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&h->dD), h->bytesD);
-    if (e == cudaErrorMemoryAllocation) {
-        cudaGetLastError();
-        return fail(h, QAP_E_CAPACITY, "block-layout buffer: cudaMalloc failed");
-    }
-    return e != cudaSuccess ? cuda_fail(h, e, "cudaMalloc") : QAP_OK;
-}
-// make layout `want` (1: stored blocks dD, 2: class layout dX) hold the current D,
-// converting on the handle's stream (never inside a graph capture)
-static qap_status d_layout(qap_rlt2 *h, int want)
-{
-    if (want == 1) {
-        qap_status s = ensure_dD(h);
-        if (s != QAP_OK) return s;
-    }
-    if (h->d_zero) {  // lazily zero: both layouts hold it
-        h->dvalid = 3;
-        return QAP_OK;
-    }
-    if (h->dvalid & want) return QAP_OK;
-    if (!(h->dvalid & 3) || (want == 2 && !h->dX)) return fail(h, QAP_E_STATE, "no layout holds D");
-    cudaError_t e = launch_xconv(h->geom, h->dD, h->dX, want == 2, h->num_sms, h->stream);
-    if (e != cudaSuccess) return cuda_fail(h, e, "layout conversion");
-    h->dvalid |= want;
-    return QAP_OK;
-}
-// before enqueueing iterations: the layout the kernels of this node use holds D
-static qap_status prepare_layout(qap_rlt2 *h)
-{
-    if (h->world > 1 || h->loopback) return QAP_OK;
-    return d_layout(h, use_x(h) ? 2 : 1);
-}
-
+// Enqueue one phase of Algorithm 1.  `st` is the stream the call's work is ordered on.
 static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused)
 {
     cudaError_t e = cudaSuccess;
@@ -736,75 +620,37 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
     switch (phase) {
     case QAP_PHASE_ITER0:
         e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
+            return launch_lap_level(LAP_L1_ACC, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         if (e) return e;
         e = launch(h, QAP_K_LAP0, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
+            return launch_lap_level(LAP_L0_ITER0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         break;
     case QAP_PHASE_TRANSFER:
     case QAP_PHASE_CONC_D: {
-        // bound() enqueues TRANSFER and CONC_D together (fused = true) so that, with
-        // QAP_FLAG_OVERLAP, they run concurrently; qap_rlt2_step runs them one at a time.
-        const bool ov = fused && (h->flags & QAP_FLAG_OVERLAP) != 0;
-        cudaStream_t sT = ov ? h->sT : st, sL = ov ? h->sL : st;
+        // bound() enqueues TRANSFER and CONC_D together (fused = true); qap_rlt2_step runs
+        // them one at a time.
         if (phase == QAP_PHASE_TRANSFER) {
-            if (ov) {
-                if ((e = cudaEventRecord(h->evJoin, st)) != cudaSuccess) return e;
-                if ((e = cudaStreamWaitEvent(sT, h->evJoin, 0)) != cudaSuccess) return e;
-            }
-            e = launch(h, QAP_K_SIGMA, sT, [&](cudaStream_t s) {
+            e = launch(h, QAP_K_SIGMA, st, [&](cudaStream_t s) {
                 return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->dSched, s);
             });
             if (e) return e;
-            if (ov) {
-                if ((e = cudaEventRecord(h->evS, sT)) != cudaSuccess) return e;
-                if ((e = cudaStreamWaitEvent(sL, h->evS, 0)) != cudaSuccess) return e;
-            }
-            TransferArgs A = transfer_args(h, ov ? 1 : 0);
-            const bool xl = !ov && use_x(h);
-            if (xl && fused && (h->flags & QAP_FLAG_FUSED) && g.n - 2 <= 32) {
-                // transfer + level-2 LAPs in one persistent kernel (k_fused_x)
-                A.D = h->dX;
-                e = launch(h, QAP_K_LAP2, sT, [&](cudaStream_t s) {
-                    return launch_fused_x(g, A, h->dX, h->dC, h->dCtl, h->dSched, h->num_sms, h->xa, h->xb,
-                                          h->xrow, s);
-                });
-                if (e) return e;
-                h->d_zero = 0;
-                h->dvalid = 2;
-                h->b_zero = 1;
-                h->c_zero = 0;
-                break;
-            }
-            const bool tma = !xl && !ov && !(h->flags & QAP_FLAG_LDG_TRANSFER) && tma_maps(h);
-            if (xl) A.D = h->dX;
-            e = launch(h, QAP_K_TRANSFER, sT, [&](cudaStream_t s) {
-                return xl ? launch_transfer_x(A, h->xmap, s)
-                          : (tma ? launch_transfer_tma(A, h->tma, s) : launch_transfer(A, 0, s));
+            TransferArgs A = transfer_args(h);
+            const bool tma = !(h->flags & QAP_FLAG_LDG_TRANSFER) && tma_maps(h);
+            e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) {
+                return tma ? launch_transfer_tma(A, h->tma, s) : launch_transfer(A, 0, s);
             });
             if (e) return e;
             h->d_zero = 0;
-            h->dvalid = xl ? 2 : 1;
             h->b_zero = h->c_zero = 1;
             if (!fused) break;
         }
-        // overlapped: at most 16 LAP warps per SM so that transfer CTAs stay co-resident
-        // (LAP warps spin on the transfer's progress counters; co-residency => progress)
-        int cfg = h->lap_warps;
-        if (ov) cfg = (cfg & ~0xf0ff) | ((cfg & 0xff) && (cfg & 0xff) < 16 ? (cfg & 0xff) : 16);
-        const bool xl = !ov && use_x(h);
-        e = launch(h, QAP_K_LAP2, sL, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, cfg, h->dSched,
-                                    ov ? 1 : 0, s, xl ? h->dX : nullptr, &h->xrow);
+        e = launch(h, QAP_K_LAP2, st, [&](cudaStream_t s) {
+            return launch_lap_level(LAP_L2, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, h->lap_warps,
+                                    h->dSched, s);
         });
         if (e) return e;
-        h->dvalid = xl ? 2 : 1;
-        if (ov) {  // LAP2 finishes after the transfer (it waited for every facility)
-            if ((e = cudaEventRecord(h->evL, sL)) != cudaSuccess) return e;
-            if ((e = cudaStreamWaitEvent(st, h->evL, 0)) != cudaSuccess) return e;
-        }
         h->c_zero = 0;
         break;
     }
@@ -812,13 +658,13 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
         // transfer between complementary costs of C: both members hold the same S after
         // CONC_D, so the pair mean is an exact no-op (reading R13); then concentrate C->B.
         e = launch(h, QAP_K_LAP1, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
+            return launch_lap_level(LAP_L1_SET, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         h->b_zero = 0;
         break;
     case QAP_PHASE_CONC_B:
         e = launch(h, QAP_K_LAP0, st, [&](cudaStream_t s) {
-            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, 0, s);
+            return launch_lap_level(LAP_L0, g, h->dD, h->dC, h->dB, h->dCtl, h->dTrace, h->num_sms, 0, nullptr, s);
         });
         break;
     default: return cudaErrorInvalidValue;
@@ -843,10 +689,6 @@ qap_status qap_rlt2_step(qap_rlt2 *h, int32_t phase)
     const int expect = h->next_phase == PH_FRESH ? QAP_PHASE_ITER0 : h->next_phase;
     if (phase != expect) return fail(h, QAP_E_STATE, "phases must run in Algorithm-1 order");
     h->call_launches = 0;
-    if (phase == QAP_PHASE_TRANSFER || phase == QAP_PHASE_CONC_D) {
-        qap_status s = prepare_layout(h);
-        if (s != QAP_OK) return s;
-    }
     cudaError_t e = launch_ctl_begin(h->dCtl, 0.0, INFINITY, h->trace_cap, h->stream);
     if (e == cudaSuccess) e = run_phase(h, phase, h->stream, false);
     if (e != cudaSuccess) return cuda_fail(h, e, "step");
@@ -873,10 +715,6 @@ qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double
     if (h->loopback) return fail(h, QAP_E_STATE, "in-process group member: use qap_rlt2_group_bound");
     if (h->geom.n < 3) return fail(h, QAP_E_STATE, "the handle holds no node");
     h->call_launches = 0;
-    if (max_iters > 0) {
-        qap_status s = prepare_layout(h);
-        if (s != QAP_OK) return s;
-    }
     cudaError_t e = launch_ctl_begin(h->dCtl, K, UB, h->trace_cap, h->stream);
     h->call_launches++;
     if (e != cudaSuccess) return cuda_fail(h, e, "ctl");
@@ -886,8 +724,8 @@ qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double
     }
     // The iteration loop is replayed from a CUDA graph (one launch instead of 5 per
     // iteration: the B&B's small nodes are launch-bound), except when per-kernel event
-    // timing, the overlap mode or sharding is on.
-    const bool graphable = h->world == 1 && !(h->flags & (QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP | QAP_FLAG_NO_GRAPH));
+    // timing or sharding is on.
+    const bool graphable = h->world == 1 && !(h->flags & (QAP_FLAG_TIME_KERNELS | QAP_FLAG_NO_GRAPH));
     if (graphable && max_iters > 0) {
         const auto key = std::make_tuple(h->geom.n, max_iters, h->d_zero);
         auto it = h->graphs.find(key);
@@ -915,7 +753,6 @@ qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double
         h->call_launches += 4 * max_iters;  // kernels in the graph: sigma, transfer, lap2, lap1, lap0
         h->call_launches += max_iters;
         h->d_zero = 0;
-        h->dvalid = use_x(h) ? 2 : 1;  // the replayed kernels wrote D in this layout
         h->b_zero = h->c_zero = 0;
     } else {
         for (int t = 0; t < max_iters; t++) {
@@ -1055,11 +892,6 @@ qap_status qap_rlt2_dual_copy(const qap_rlt2 *hc, double *B, double *C, double *
         else if ((e = cudaMemcpy2D(C, w, h->dC, g.ldc * 8, w, n * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
             return cuda_fail(h, e, "copy C");
     }
-    if (D && h->world == 1 && !h->loopback && !h->d_zero && !(h->dvalid & 1)) {
-        qap_status s = d_layout(h, 1);  // export layout: stored blocks
-        if (s != QAP_OK) return s;
-        if ((e = cudaStreamSynchronize(h->stream)) != cudaSuccess) return cuda_fail(h, e, "sync");
-    }
     if (D) {
         const size_t w = (size_t)(n - 2) * (n - 2) * 8;
         // sharded: only this rank's blocks (at their global positions); the rest is untouched
@@ -1161,6 +993,7 @@ struct Bnb {
     // node with base_m + d fixed pairs on the current DFS path (depth[0] = the caller's handle)
     bool warm = false;
     int base_m = 0;
+    std::vector<int32_t> root_fac, root_loc;  // the subtree root's fixed pairs (base_m of them)
     std::vector<qap_rlt2 *> depth;
     // warm: pool handle j holds the post-bound state of child holds[j].second of the frame
     // with id holds[j].first (until the handle is reused): expanding that child copies it
@@ -1481,7 +1314,7 @@ qap_status Bnb::depth_handle(size_t d)
             qap_rlt2_opts op{};
             op.device = own->device;
             op.cuda_stream = own->stream;
-            op.flags = own->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP);
+            op.flags = own->flags & ~QAP_FLAG_TIME_KERNELS;
             op.lap_warps = own->lap_warps;
             qap_rlt2 *x = nullptr;
             const int cap = own->N - (int)kk;
@@ -1502,10 +1335,6 @@ qap_status Bnb::copy_state(qap_rlt2 *dst, const qap_rlt2 *src)
     const Geom &g = src->geom;
     if (g.n > dst->n_cap) return fail(dst, QAP_E_CAPACITY, "state copy: node larger than the target");
     cudaError_t e;
-    qap_rlt2 *s0 = const_cast<qap_rlt2 *>(src);
-    qap_status ls = d_layout(s0, 1);  // copies go through the stored-block layout
-    if (ls != QAP_OK) return fail(dst, ls, "state copy: " + s0->err);
-    if ((ls = ensure_dD(dst)) != QAP_OK) return ls;
     if ((e = cudaEventRecord(src->evJoin, src->stream)) != cudaSuccess ||
         (e = cudaStreamWaitEvent(dst->stream, src->evJoin, 0)) != cudaSuccess)
         return cuda_fail(dst, e, "state copy ordering");
@@ -1526,14 +1355,14 @@ qap_status Bnb::copy_state(qap_rlt2 *dst, const qap_rlt2 *src)
     dst->geom = src->geom;
     dst->next_phase = src->next_phase;
     dst->d_zero = src->d_zero;
-    dst->dvalid = src->d_zero ? 3 : 1;
     dst->b_zero = src->b_zero;
     dst->c_zero = src->c_zero;
     return QAP_OK;
 }
 
-// ---- checkpoint file (binary, little-endian; written to <path>.tmp then renamed) --------
+// ---- checkpoint file (binary, little-endian; written to <path>.tmp, fsync'ed, renamed) ----
 constexpr uint64_t kCkptMagic = 0x3254504b32544c52ull;  // "RLT2KPT2"
+constexpr uint32_t kCkptVersion = 3;  // 3: + format version, subtree root (base_m, its pairs)
 
 uint64_t instance_digest(const qap_rlt2 *h)
 {
@@ -1599,6 +1428,7 @@ bool save_checkpoint(const Bnb &B, const char *path, std::string &err)
 {
     std::vector<char> o;
     put(o, kCkptMagic);
+    put(o, kCkptVersion);
     put(o, instance_digest(B.h0()));
     put(o, (int32_t)B.N);
     put(o, (int32_t)B.iters);
@@ -1606,6 +1436,9 @@ bool save_checkpoint(const Bnb &B, const char *path, std::string &err)
     put(o, (int32_t)B.warm);
     put(o, B.K);
     put(o, B.UB0);
+    put(o, (int32_t)B.base_m);
+    putv(o, B.root_fac);
+    putv(o, B.root_loc);
     put(o, B.UB);
     put(o, (uint8_t)B.have);
     put(o, B.best);
@@ -1631,11 +1464,21 @@ bool save_checkpoint(const Bnb &B, const char *path, std::string &err)
         err = "cannot open " + tmp;
         return false;
     }
-    const bool wrote = fwrite(o.data(), 1, o.size(), f) == o.size() && fflush(f) == 0;
+    // the data reaches the disk before the rename publishes it (a crash leaves either the
+    // old checkpoint or the new one, never a truncated file under `path`)
+    const bool wrote = fwrite(o.data(), 1, o.size(), f) == o.size() && fflush(f) == 0 && fsync(fileno(f)) == 0;
     fclose(f);
     if (!wrote || rename(tmp.c_str(), path) != 0) {
         err = "cannot write checkpoint " + std::string(path);
         return false;
+    }
+    std::string dir(path);
+    const size_t slash = dir.find_last_of('/');
+    dir = slash == std::string::npos ? "." : (slash == 0 ? "/" : dir.substr(0, slash));
+    const int dfd = open(dir.c_str(), O_RDONLY);
+    if (dfd >= 0) {  // the rename itself (best effort: some file systems refuse directory fsync)
+        fsync(dfd);
+        close(dfd);
     }
     return true;
 }
@@ -1657,10 +1500,20 @@ bool load_checkpoint(Bnb &B, const char *path, std::string &err)
         err = "not a checkpoint file";
         return false;
     }
+    if (R.get<uint32_t>() != kCkptVersion) {
+        err = "checkpoint format version mismatch";
+        return false;
+    }
     if (R.get<uint64_t>() != instance_digest(B.h0()) || R.get<int32_t>() != B.N || R.get<int32_t>() != B.iters ||
         R.get<int32_t>() != B.sb_iters || R.get<int32_t>() != (int32_t)B.warm || R.get<double>() != B.K ||
         R.get<double>() != B.UB0) {
         err = "checkpoint belongs to another instance or parameters";
+        return false;
+    }
+    const int32_t base_m = R.get<int32_t>();
+    const std::vector<int32_t> rf = R.getv<int32_t>(), rl = R.getv<int32_t>();
+    if (!R.ok || base_m != B.base_m || rf != B.root_fac || rl != B.root_loc) {
+        err = "checkpoint belongs to another subtree root";
         return false;
     }
     B.UB = R.get<double>();
@@ -1688,6 +1541,21 @@ bool load_checkpoint(Bnb &B, const char *path, std::string &err)
     if (!R.ok) {
         err = "truncated checkpoint";
         return false;
+    }
+    // frame k is the expanded node at depth base_m + k on the DFS path, below the root
+    for (size_t k = 0; k < B.stack.size(); k++) {
+        const Frame &F = B.stack[k];
+        bool ok = F.fac.size() == (size_t)B.base_m + k && F.loc.size() == F.fac.size() &&
+                  F.ls.size() == F.fs.size() && F.est.size() == F.fs.size() && F.lb.size() == F.fs.size() &&
+                  F.next <= F.fs.size() && F.fac.size() < (size_t)B.N;
+        for (size_t t = 0; ok && t < (size_t)B.base_m; t++)
+            ok = F.fac[t] == B.root_fac[t] && F.loc[t] == B.root_loc[t];
+        for (size_t t = 0; ok && t < F.fac.size(); t++)
+            ok = F.fac[t] >= 0 && F.fac[t] < B.N && F.loc[t] >= 0 && F.loc[t] < B.N;
+        if (!ok) {
+            err = "inconsistent checkpoint stack";
+            return false;
+        }
     }
     B.root_done = true;
     return true;
@@ -1719,6 +1587,10 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
     b.warm = o->warm != 0;
     if (b.warm && h->world > 1) return fail(h, QAP_E_ARG, "warm B&B needs a single-GPU handle");
     b.base_m = o->root ? o->root->m : 0;
+    if (o->root) {
+        b.root_fac.assign(o->root->fac, o->root->fac + o->root->m);
+        b.root_loc.assign(o->root->loc, o->root->loc + o->root->m);
+    }
     b.depth.push_back(h);
     const int B = o->batch < 1 ? 1 : (o->batch > b.N ? b.N : o->batch);
     const int nh = b.warm ? B : B - 1;  // warm: the caller's handle keeps the root's state
@@ -1729,7 +1601,7 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
         qap_rlt2_opts op{};
         op.device = h->device;
         op.cuda_stream = s;
-        op.flags = h->flags & ~(QAP_FLAG_TIME_KERNELS | QAP_FLAG_OVERLAP);
+        op.flags = h->flags & ~QAP_FLAG_TIME_KERNELS;
         op.lap_warps = h->lap_warps;
         qap_rlt2 *x = nullptr;
         qap_status st = qap_rlt2_create(h->N, h->F.data(), h->Dist.data(), &op, &x);

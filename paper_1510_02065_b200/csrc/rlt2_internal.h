@@ -25,13 +25,10 @@ struct Ctl {
     int pad;
 };
 
-// Cross-kernel schedule of one iteration (overlap of transfer and level-2 LAPs):
-// done[a] counts finished transfer CTAs whose facility triple has smallest facility a;
-// head is the level-2 LAP work queue.  Reset by k_sigma every iteration.
+// The level-2 LAP work queue (blocks handed out in order to persistent warps); reset by
+// k_sigma every iteration.
 struct Sched {
-    unsigned done[kMaxN];
     unsigned long long head;
-    unsigned long long thead;  // fused iteration (k_fused_x): transfer-tile queue
 };
 
 // Geometry of the reduced problem at the current node.
@@ -41,9 +38,6 @@ struct Geom {
     int64_t ld2;       // stride (doubles) of one stored D block: (n-2)^2 rounded up to even
     int64_t nblk;      // stored D blocks n^2 (n-1)^2 / 2
     int64_t off[kMaxN + 1];  // first block id of facility i (canonical first facility)
-    // class layout X: 3 member sections of ntri facility triples, each an
-    // n x n x np array [first location][second location][row facility's location]
-    int np;            // innermost stride: n rounded up to even (16-byte aligned rows)
     int ntri;          // facility triples n (n-1) (n-2) / 6
 };
 
@@ -66,16 +60,8 @@ inline void make_geom(int n, Geom &g)
         g.off[i] = acc;
         if (i < n) acc += (int64_t)n * (n - 1 - i) * (n - 1);
     }
-    g.np = (n + 1) & ~1;
     g.ntri = n * (n - 1) * (n - 2) / 6;
 }
-// doubles of the class layout X for node size n (3 sections of ntri * n * n * np)
-inline size_t x_doubles(int n)
-{
-    const int64_t np = (n + 1) & ~1, ntri = (int64_t)n * (n - 1) * (n - 2) / 6;
-    return (size_t)(3 * ntri * n * n * np);
-}
-constexpr int kXMin = 16;  // smallest node size bounded in the class layout
 
 // LAP launch levels.
 enum LapLevel { LAP_L2 = 0, LAP_L1_ACC = 1, LAP_L1_SET = 2, LAP_L0_ITER0 = 3, LAP_L0 = 4, LAP_BATCH = 5,
@@ -135,7 +121,6 @@ struct TransferArgs {
     Sched *sched;
     int ntile;            // ceil(n / TT)
     unsigned ntile_mul;   // ceil(2^16 / ntile): y / ntile = (y * ntile_mul) >> 16 for y < 64 (set by the launcher)
-    int publish;          // overlapped mode: publish per-facility progress
     // sharded iteration (nullptr tiles: every tile, single rank)
     const int *tiles;     // this rank's tiles (global tile id = triple * ntile^3 + tile)
     const int *tinfo;     // kind | slot << 2 (slot: 512-double unit of the exchange buffers)
@@ -152,18 +137,6 @@ struct TmaMaps {
     CUtensorMap m[kMaxN];
 };
 cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStream_t st);
-// class layout X: the transfer as tensor-map box load -> class mean -> box store (A.D = X;
-// xmap: 4-D map [np][n][n][3 ntri] of X with 8x8x8x1 boxes)
-cudaError_t launch_transfer_x(const TransferArgs &A, const CUtensorMap &xmap, cudaStream_t st);
-// stored blocks <-> class layout X (to_x = 1: D -> X; 0: X -> D); valid entries only
-cudaError_t launch_xconv(const Geom &g, double *D, double *X, int to_x, int num_sms, cudaStream_t st);
-// One iteration's transfer and level-2 concentration in one persistent kernel over the class
-// layout (QAP_FLAG_FUSED): warps take 4x8x8 transfer tiles or level-2 LAPs
-// whose facility's transfer has completed.  xa / xb: 4-D maps of X with {8,8,4,1} / {4,8,8,1}
-// boxes; xrow: the 2-D row map of the level-2 LAP (gather4 / scatter4).
-cudaError_t launch_fused_x(const Geom &g, const TransferArgs &A, double *X, double *C, Ctl *ctl, Sched *sched,
-                           int num_sms, const CUtensorMap &xa, const CUtensorMap &xb, const CUtensorMap &xrow,
-                           cudaStream_t st);
 int tma_box0(int n);  // dim0 box extent for node size n (TT + 2 when n - 2 is even, else TT + 4)
 struct Offsets {
     int64_t off[kMaxN];
@@ -171,12 +144,10 @@ struct Offsets {
 cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, double *C, const Ctl *ctl,
                           cudaStream_t st);
 // Level-2 / level-1 / level-0 concentrations (one warp per LAP).
-// sched != nullptr (level 2 only): blocks come from the Sched queue in facility order and
-// wait for the transfer of their facility (concurrent-kernel overlap).
+// sched != nullptr (level 2 only): persistent warps take blocks from the Sched queue.
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B,
                              Ctl *ctl, double *trace, int num_sms, int lap_warps, Sched *sched,
-                             int wait, cudaStream_t st, double *X = nullptr,
-                             const CUtensorMap *xrow = nullptr);
+                             cudaStream_t st);
 // Level-2 LAPs of `count` local blocks (sharded): S of block b to Sout[b].
 cudaError_t launch_lap_l2_local(const Geom &g, double *Dloc, int64_t count, double *Sout, Ctl *ctl, int num_sms,
                                 int lap_cfg, Sched *sched, cudaStream_t st);

@@ -122,35 +122,6 @@ __device__ __forceinline__ int64_t bid_of(const Geom &g, int i, int j, int k, in
     return g.off[i] + (int64_t)j * (n1 - i) * n1 + (int64_t)(k - i - 1) * n1 + (l - (l > j));
 }
 
-// Class layout X (see k_transfer_x): row runs of stored blocks.
-__device__ __forceinline__ int tri_index(int n, int a, int b, int c)
-{
-    const int A = n - a, K = A - 1, bb = b - a - 1, Kb = K - bb;
-    return (n * (n - 1) * (n - 2) - A * (A - 1) * (A - 2)) / 6 + (K * (K - 1) - Kb * (Kb - 1)) / 2 + (c - b - 1);
-}
-// row p (p != i, k) of stored block D{ij,kl} (i < k): index of its run in units of np doubles
-__device__ __forceinline__ unsigned x_row(const Geom &g, int i, int j, int k, int l, int p)
-{
-    int r, t;
-    if (p > k) { r = 0; t = tri_index(g.n, i, k, p); }
-    else if (p > i) { r = 1; t = tri_index(g.n, i, p, k); }
-    else { r = 2; t = tri_index(g.n, p, i, k); }
-    return ((unsigned)(r * g.ntri + t) * (unsigned)g.n + (unsigned)j) * (unsigned)g.n + (unsigned)l;
-}
-// location of column s of a block whose pairs hold locations j and l (reading R7)
-__device__ __forceinline__ int x_col(int s, int j, int l)
-{
-    const int lo = j < l ? j : l, hi = j < l ? l : j;
-    const int q = s + (s >= lo);
-    return q + (q >= hi);
-}
-// facility of row r of a block whose pairs hold facilities i < k
-__device__ __forceinline__ int x_rowfac(int r, int i, int k)
-{
-    const int p = r + (r >= i);
-    return p + (p >= k);
-}
-
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -248,32 +219,104 @@ __device__ __forceinline__ T sel_t(const T (&a)[CPL], int t)
     return (CPL == 1 || t == 0) ? a[0] : a[CPL - 1];
 }
 
-// Solve the m×m LAP whose row-major costs start at Mlane - lane (shared memory).
+// Munkres' row reduction (reading R4, oracle O2): u_r = min_s M[r][s] for every row,
+// v = 0, and the initial partial assignment on the zeros this creates — row r takes the
+// lowest column attaining its minimum unless a lower row took that column.  Lane `lane`
+// scans rows lane + 32 u (a row of a lane without one: row 0, unused); `col[t]` is the column
+// of the lane's owned slot t.  Returns the row minima (rmin[u] of row lane + 32 u), the masks
+// of matched rows (bit r & 31 of rmask[r >> 5]) and, per owned column, poff / ucol of its
+// matched row (-1 / 0 when free).  `colrow` is m ints of per-warp shared scratch.
+template <int CPL>
+__device__ __forceinline__ void munkres_init(const double *M, int m, int lane, const int (&col)[CPL], int *colrow,
+                                             int (&poff)[CPL], double (&ucol)[CPL], double (&rmin)[CPL],
+                                             uint32_t (&rmask)[CPL])
+{
+    const int rowb = m * 8;
+    int rarg[CPL];
+#pragma unroll
+    for (int u = 0; u < CPL; u++) {
+        const int r = lane + 32 * u;
+        const double *rp = M + (r < m ? r : 0) * m;
+        double mn = rp[0];
+        int am = 0;
+#pragma unroll 4
+        for (int c = 1; c < m; c++) {  // strict <: the lowest column among equal minima
+            const double x = rp[c];
+            if (x < mn) {
+                mn = x;
+                am = c;
+            }
+        }
+        rmin[u] = mn;
+        rarg[u] = am;
+    }
+#pragma unroll
+    for (int t = 0; t < CPL; t++)
+        if (col[t] < m) colrow[col[t]] = -1;
+    __syncwarp();
+    // one writer per column within a group of 32 rows (the lowest lane of each match group);
+    // the lower group writes last, so the lowest row holding a column's minimum keeps it
+#pragma unroll
+    for (int u = CPL - 1; u >= 0; u--) {
+        const int r = lane + 32 * u;
+        const uint32_t grp = __match_any_sync(FULL_MASK, r < m ? rarg[u] : 64 + lane);
+        if (r < m && (grp & ((1u << lane) - 1u)) == 0u) colrow[rarg[u]] = r;
+        __syncwarp();
+    }
+#pragma unroll
+    for (int u = 0; u < CPL; u++) {
+        const int r = lane + 32 * u;
+        rmask[u] = __ballot_sync(FULL_MASK, r < m && colrow[rarg[u]] == r);
+    }
+#pragma unroll
+    for (int t = 0; t < CPL; t++) {
+        const int r = col[t] < m ? colrow[col[t]] : -1;
+        const int src = r < 0 ? 0 : r;
+        double ur = __shfl_sync(FULL_MASK, rmin[0], src & 31);
+        if (CPL > 1) {
+            const double ur1 = __shfl_sync(FULL_MASK, rmin[CPL - 1], src & 31);
+            if (src >= 32) ur = ur1;
+        }
+        poff[t] = r < 0 ? -1 : r * rowb;
+        ucol[t] = r < 0 ? 0.0 : ur;
+    }
+    __syncwarp();  // the scratch is free again
+}
+
+// Solve the m×m LAP whose row-major costs start at M (shared memory): Munkres' row
+// reduction, then the rows left are inserted in ascending order, each by one
+// shortest-augmenting-path search.  Lane `lane` owns columns lane + 32 t.
 // Outputs per owned column: poff (matched row × 8m bytes), v, ucol.
 template <int CPL, bool COUNT>
-__device__ __forceinline__ void warp_lap_solve(const double *Mlane, int m, int lane, int (&poff)[CPL],
+__device__ __forceinline__ void warp_lap_solve(const double *M, int m, int lane, int *scratch, int (&poff)[CPL],
                                                double (&v)[CPL], double (&ucol)[CPL], int &steps)
 {
+    const double *Mlane = M + lane;
     double minv[CPL];
     double du[CPL];  // 1.0 on settled columns, else 0.0: fma(delta, du, x) == x + delta exactly
     int way[CPL];
     const int rowb = m * 8;
+    int col[CPL];
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         v[t] = 0.0;
-        ucol[t] = 0.0;
-        poff[t] = -1;
         way[t] = -1;
+        col[t] = lane + 32 * t;
     }
+    double rmin[CPL];
+    uint32_t rmask[CPL];
+    munkres_init<CPL>(M, m, lane, col, scratch, poff, ucol, rmin, rmask);
     for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
-        double ucur = 0.0;         // u of row i = u[p[dummy]]
+        if ((sel_t<CPL>(rmask, i >> 5) >> (i & 31)) & 1u) continue;  // matched by the row reduction
+        // u of row i = u[p[dummy]]: its row minimum
+        double ucur = __shfl_sync(FULL_MASK, sel_t<CPL>(rmin, i >> 5), i & 31);
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             minv[t] = (lane + 32 * t) < m ? CUDART_INF : qnan();
             du[t] = 0.0;
         }
         int j0 = -1, i0off = i * rowb;
-        double ui0 = 0.0;
+        double ui0 = ucur;
         int jfree;
         while (true) {
             const double *row = reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off);
@@ -388,19 +431,28 @@ __device__ __noinline__ uint32_t argmin_keyed(double minv)
     return bal;
 }
 template <bool COUNT>
-__device__ __forceinline__ void warp_lap_solve1(const double *Mlane, int m, int ldm, int lane, int &poff, double &v,
+__device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane, int *scratch, int &poff, double &v,
                                                 double &ucol, int &steps)
 {
+    const double *Mlane = M + (31 - lane);
     v = 0.0;
-    ucol = 0.0;
-    poff = -1;
     int way = -1;
-    const int rowb = ldm * 8;  // bytes per cost row
+    const int rowb = m * 8;  // bytes per cost row
     double minv0 = 31 - lane < m ? CUDART_INF : qnan();
     asm("" : "+d"(minv0));  // keep it in registers (not rematerialised per row)
-    uint32_t freemask = m >= 32 ? 0xffffffffu : ~((1u << (32 - m)) - 1u);  // lanes 32-m .. 31
+    int pc[1], col[1] = {31 - lane};
+    double uc[1], rm[1];
+    uint32_t rmask[1];
+    munkres_init<1>(M, m, lane, col, scratch, pc, uc, rm, rmask);
+    poff = pc[0];
+    ucol = uc[0];
+    const double rmin = rm[0];
+    // lanes 32-m .. 31 hold columns; those matched by the row reduction are taken
+    uint32_t freemask = (m >= 32 ? 0xffffffffu : ~((1u << (32 - m)) - 1u)) & ~__ballot_sync(FULL_MASK, poff >= 0);
     for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
-        double ucur = 0.0, ui0 = 0.0, minv = minv0, du = 0.0;
+        if ((rmask[0] >> i) & 1u) continue;  // matched by the row reduction
+        const double ui = __shfl_sync(FULL_MASK, rmin, i);  // u of row i: its row minimum
+        double ucur = ui, ui0 = ui, minv = minv0, du = 0.0;
         int j0 = -1, i0off = i * rowb, j1;
 #pragma unroll 2
         for (;;) {
@@ -531,26 +583,19 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, GVal Mg, int m, i
     return S;
 }
 
-// Shared memory per warp: NBUF cost buffers (TMA destinations; m*m doubles plus 32*CPL
+// Shared memory per warp: the cost buffer (TMA destination; m*m doubles plus 32*CPL - m
 // doubles of padding so that every lane may load its column of any row unconditionally),
-// urow[m], sel[m], 2 mbarriers — packed tightly so that 32 warps fit one SM at m = 28.
-// ldrow > 0: the class layout with one column per lane (rows of ldrow doubles moved whole by
-// per-lane TMA bulk copies; columns are per-lane offsets, lanes without one read a junk slot)
-__host__ __device__ inline size_t lap_buf_bytes(int m, int cpl, int ldrow = 0)
+// urow[m], sel[m], one mbarrier — packed tightly so that 34 warps fit one SM at m = 28.
+__host__ __device__ inline size_t lap_buf_bytes(int m, int cpl)
 {
-    if (ldrow > 0) return ((size_t)m * ldrow * 8 + 15) & ~size_t(15);
     // lanes without a column read entry (r, c >= m) of any row r: the block plus 32 cpl - m
     // doubles of padding keeps every such read inside the buffer
     const int pad = 32 * cpl > m ? 32 * cpl - m : 0;
     return (((size_t)m * m + pad) * 8 + 15) & ~size_t(15);
 }
-__host__ __device__ inline size_t lap_warp_smem(int m, int cpl, int nbuf, int ldrow = 0)
+__host__ __device__ inline size_t lap_warp_smem(int m, int cpl)
 {
-    // ldrow > 0 (class layout, one column per lane): rows in groups of 4 moved by TMA gather4 /
-    // scatter4 (128-byte aligned groups: ldrow % 4 == 0), u and the selected entry of row r kept
-    // in the row's spare columns n and n + 1 (ldrow >= n + 2), one mbarrier per warp at the end
-    if (ldrow > 0) return (size_t)((m + 3) & ~3) * ldrow * 8 + 16;
-    return nbuf * lap_buf_bytes(m, cpl) + (((size_t)2 * m * 8 + 15) & ~size_t(15)) + 16;
+    return lap_buf_bytes(m, cpl) + (((size_t)2 * m * 8 + 15) & ~size_t(15)) + 16;
 }
 
 // First (canonical) facility of stored block b; `hint` only moves forward.
@@ -571,51 +616,14 @@ struct LapArgs {
     Ctl *ctl;
     double *trace;
     LapBatchOut bo;
-    Sched *sched;  // non-null: dynamic queue + wait for the transfer of each block's facility
-    int ntile3;    // transfer CTAs per facility triple
+    Sched *sched;  // non-null: dynamic work queue (head reset by k_sigma)
     int64_t bdiv, bstr;  // level 1: B index of block b = (b / bdiv) * bstr + b % bdiv (batched RLT1)
     double *lbm;         // LAP_L0_MULTI: lbm[b] += S
     int chunk;           // dynamic mode: blocks per work-queue grab (set by the launcher)
     // level 2: x / d = umulhi(x, ceil(2^32 / d)) (exact for x d < 2^32) for d = n - 1 and
     // d = (n - 1 - i)(n - 1), the block-id decode of the S credit (no integer division)
     uint32_t mag_n1, mag_pj[kMaxN];
-    double *X;  // level 2 in the class layout (k_lap<..., XL = true>): blocks are row runs of X
-    const CUtensorMap *xrow;  // host: 2-D map [3 ntri n n][np] of X with {np, 1} boxes (gather4)
 };
-// TMA tile::gather4 / tile::scatter4 (sm_100a): four row runs of X <-> four consecutive
-// rows of the cost buffer in one instruction (2-D row map, box {ldm, 1}, coordinates
-// {0, rows}).  All row groups of one block: lane 0 issues one gather4 (load) or scatter4
-// (store) per 4 rows; row r's run index is held by lane r (x_rows), rows >= m by junk row 0.
-template <bool LOAD>
-__device__ __forceinline__ void x_rows4(const CUtensorMap *tm, double *M, int ldm, int m4, unsigned xr, int lane,
-                                        uint64_t *mbar)
-{
-    const uint64_t tma = reinterpret_cast<uint64_t>(tm);
-    uint32_t sa = smem_u32(M);
-    const uint32_t gstep = (uint32_t)(4 * ldm * 8);
-    const uint32_t mb = smem_u32(mbar);
-#pragma unroll 1
-    for (int r = 0; r < m4; r += 4) {
-        const unsigned r0 = __shfl_sync(FULL_MASK, xr, r), r1 = __shfl_sync(FULL_MASK, xr, r + 1),
-                       r2 = __shfl_sync(FULL_MASK, xr, r + 2), r3 = __shfl_sync(FULL_MASK, xr, r + 3);
-        if (lane == 0) {
-            if (LOAD)
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], "
-                    "[%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(sa),
-                    "l"(tma), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(mb)
-                    : "memory");
-            else
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], "
-                    "[%6];" ::"l"(tma),
-                    "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(sa)
-                    : "memory");
-        }
-        sa += gstep;
-    }
-}
-
 // Level 2: pairs (i,j), (k,l) of stored block b (i = canonical first facility; `icur` is a
 // hint that only moves forward), packed i | j << 8 | k << 16 | l << 24.
 __device__ __forceinline__ unsigned decode_l2(const LapArgs &a, int64_t b, int &icur)
@@ -633,113 +641,11 @@ __device__ __forceinline__ unsigned decode_l2(const LapArgs &a, int64_t b, int &
     return (unsigned)icur | ((unsigned)j << 8) | ((unsigned)k << 16) | ((unsigned)l << 24);
 }
 
-// Class layout: run index (units of np doubles) of the rows lane + 32 u of the block.
-template <int CPL>
-__device__ __forceinline__ void x_rows(const Geom &g, unsigned ijkl, int m, int lane, unsigned (&xr)[CPL])
-{
-    const int i = ijkl & 0xff, j = (ijkl >> 8) & 0xff, k = (ijkl >> 16) & 0xff, l = ijkl >> 24;
-#pragma unroll
-    for (int u = 0; u < CPL; u++) {
-        const int r = lane + 32 * u;
-        xr[u] = r < m ? x_row(g, i, j, k, l, x_rowfac(r, i, k)) : 0u;
-    }
-}
-// Per owned column: its slot in a row run (a lane without a column, c >= m, uses the slot of
-// location j, which belongs to no class), and its cell of row 0 in the warp's cost buffer
-// with the row stride (c >= m: a padding cell, stride 0) — branch-free row loops.
-template <int CPL>
-struct XCols {
-    const double *g[CPL];  // X + slot
-    double *s[CPL];        // cost-buffer cell of row 0
-    int ss[CPL];           // cost-buffer row stride (doubles)
-};
-template <int CPL>
-__device__ __forceinline__ void x_cols(const double *X, double *M, unsigned ijkl, int m, int col0, XCols<CPL> &xc)
-{
-    const int j = (ijkl >> 8) & 0xff, l = ijkl >> 24;
-#pragma unroll
-    for (int t = 0; t < CPL; t++) {
-        const int c = col0 + 32 * t;
-        const bool own = c < m;
-        xc.g[t] = X + (own ? x_col(c, j, l) : j);
-        xc.s[t] = own ? M + c : M + m * m + (c - m);
-        xc.ss[t] = own ? m : 0;
-    }
-}
-template <int CPL>
-__device__ __forceinline__ unsigned x_pick(const unsigned (&xr)[CPL], int r)
-{
-    unsigned v = xr[0];
-#pragma unroll
-    for (int u = 1; u < CPL; u++)
-        if ((r >> 5) == u) v = xr[u];
-    return __shfl_sync(FULL_MASK, v, r & 31);
-}
-// asynchronous row-run loads of one block into the warp's cost buffer (cp.async, 8 B/lane)
-template <int CPL>
-__device__ __forceinline__ void x_load(int np, int m, const unsigned (&xr)[CPL], const XCols<CPL> &xc)
-{
-    uint32_t sa[CPL];
-#pragma unroll
-    for (int t = 0; t < CPL; t++) sa[t] = smem_u32(xc.s[t]);
-    const uint32_t np8 = (uint32_t)np * 8u;  // u32 x u32 -> u64: one IMAD.WIDE.U32 per row
-    for (int r = 0; r < m; r++) {
-        const uint64_t off = (uint64_t)x_pick<CPL>(xr, r) * np8;
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa[t]),
-                         "l"(reinterpret_cast<const char *>(xc.g[t]) + off)
-                         : "memory");
-            sa[t] += (uint32_t)xc.ss[t] * 8u;
-        }
-    }
-    cp_async_commit();
-}
-// residual rows of the cost buffer back to their runs
-template <int CPL>
-__device__ __forceinline__ void x_store(int np, int m, const unsigned (&xr)[CPL], const XCols<CPL> &xc)
-{
-    const double *sp[CPL];
-#pragma unroll
-    for (int t = 0; t < CPL; t++) sp[t] = xc.s[t];
-    const uint32_t np8 = (uint32_t)np * 8u;  // u32 x u32 -> u64: one IMAD.WIDE.U32 per row
-    for (int r = 0; r < m; r++) {
-        const uint64_t off = (uint64_t)x_pick<CPL>(xr, r) * np8;
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            *reinterpret_cast<double *>(const_cast<char *>(reinterpret_cast<const char *>(xc.g[t])) + off) = *sp[t];
-            sp[t] += xc.ss[t];
-        }
-    }
-}
-
-
-// Lane 0 only: block until the transfer of every facility <= a has finished (acquire),
-// then order those generic-proxy writes before our async-proxy (TMA) reads.
-__device__ __forceinline__ void wait_transfer(const LapArgs &a_, int a, int &ready)
-{
-    const int n = a_.g.n;
-    unsigned spins = 0;
-    while (ready < a) {
-        const int x = ready + 1;
-        const unsigned total = (unsigned)a_.ntile3 * (unsigned)((n - 1 - x) * (n - 2 - x) / 2);
-        if (x > n - 3 || ld_acquire(&a_.sched->done[x]) >= total) {
-            ready++;
-            spins = 0;
-        } else {
-            __nanosleep(256);
-            if (++spins > (1u << 26)) __trap();  // ~20 s without progress: fail, never hang
-        }
-    }
-    fence_proxy_async_global();
-}
-
-// WAIT: overlapped mode (QAP_FLAG_OVERLAP), blocks wait for the transfer of their facility.
 // Control flow is kept provably warp-uniform for ptxas (warp index and the stop flag read
-// through a shuffle; the transfer wait loop only in the WAIT instantiation): otherwise every
-// redux/shfl of the solver is guarded by a BRA.DIV pair (~15% of the Dijkstra step's issue).
-template <int CPL, int NBUF, bool WAIT, bool XL>
-__global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_constant__ CUtensorMap xrow)
+// through a shuffle): otherwise every redux/shfl of the solver is guarded by a BRA.DIV pair
+// (~15% of the Dijkstra step's issue).
+template <int CPL>
+__global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
 {
     if (a.ctl != nullptr && __shfl_sync(FULL_MASK, a.ctl->stopped, 0)) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -747,17 +653,12 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_cons
               lane = threadIdx.x & 31;
     const int col0 = CPL == 1 ? 31 - lane : lane;  // this lane's (first) column
     const int m = a.m;
-    // XB: class layout, one column per lane: whole row runs by per-lane TMA bulk copies
-    constexpr bool XB = XL && CPL == 1;
-    const int ldm = XB ? ((a.g.n + 5) & ~3) : m;  // cost-buffer row stride (doubles); XB: >= n + 2, % 4 == 0
-    const int m4 = (m + 3) & ~3;                   // XB: rows moved in groups of 4 (gather4 / scatter4)
-    const size_t bufb = XB ? (size_t)m4 * ldm * 8 : lap_buf_bytes(m, CPL);
-    unsigned char *wbase = smem + (size_t)warp * (XB ? bufb : lap_warp_smem(m, CPL, NBUF));
-    double *urow = reinterpret_cast<double *>(wbase + NBUF * bufb);
+    const size_t bufb = lap_buf_bytes(m, CPL);
+    unsigned char *wbase = smem + (size_t)warp * lap_warp_smem(m, CPL);
+    double *urow = reinterpret_cast<double *>(wbase + bufb);
     double *sel = urow + m;
-    uint64_t *mbar = XB ? reinterpret_cast<uint64_t *>(smem + (size_t)wpc * bufb + (size_t)warp * 16)
-                        : reinterpret_cast<uint64_t *>(wbase + NBUF * bufb + (((size_t)2 * m * 8 + 15) & ~size_t(15)));
-    double *const xurow = reinterpret_cast<double *>(wbase) + a.g.n, *const xsel = xurow + 1;  // XB: spare columns
+    int *const scratch = reinterpret_cast<int *>(sel);  // the solver's row-reduction table (m ints)
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(wbase + bufb + (((size_t)2 * m * 8 + 15) & ~size_t(15)));
 
     const bool dyn = a.sched != nullptr;
     const int CH = a.chunk;  // blocks per work-queue grab (dynamic mode)
@@ -774,34 +675,13 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_cons
     }
     if (b >= a.count) return;
     const uint32_t bytes = (uint32_t)(((int64_t)m * m + 1) & ~int64_t(1)) * 8u;
-    int hint_load = 0, ready = -1;
     int icur = 0;  // canonical first facility of block b (L2), advanced monotonically
-    unsigned ijkl = 0;  // XL: pairs of block b
-    unsigned xr[CPL];   // XL: row runs of block b
     int cofs[CPL];      // offset of each owned column within a cost-buffer row
 #pragma unroll
     for (int t = 0; t < CPL; t++) cofs[t] = col0 + 32 * t;
-    if (XB) {
-        ijkl = decode_l2(a, b, icur);
-        x_rows<CPL>(a.g, ijkl, m, lane, xr);
-        if (lane == 0) {
-            mbar_init(&mbar[0], 1);
-            fence_mbar_init();
-            mbar_expect_tx(&mbar[0], (uint32_t)(m4 * ldm * 8));
-        }
-        // rows >= m: junk row 0 (locations j = l = 0)
-        x_rows4<true>(&xrow, reinterpret_cast<double *>(wbase), ldm, m4, xr[0], lane, &mbar[0]);
-    } else if (XL) {
-        ijkl = decode_l2(a, b, icur);
-        x_rows<CPL>(a.g, ijkl, m, lane, xr);
-        XCols<CPL> xc;
-        x_cols<CPL>(a.X, reinterpret_cast<double *>(wbase), ijkl, m, col0, xc);
-        x_load<CPL>(a.g.np, m, xr, xc);
-    } else if (lane == 0) {
+    if (lane == 0) {
         mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
         fence_mbar_init();
-        if (WAIT) wait_transfer(a, facility_of(a.g, b, hint_load), ready);
         mbar_expect_tx(&mbar[0], bytes);
         tma_load_1d(wbase, a.src + b * a.ld, bytes, &mbar[0]);
     }
@@ -821,94 +701,28 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_cons
         } else {
             nb = b + nw;
         }
-        const int slot = NBUF == 2 ? (it & 1) : 0;
-        if (NBUF == 2 && lane == 0 && nb < a.count) {
-            if (WAIT) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
-            bulk_wait_read();  // the residual store out of the other buffer has read it
-            mbar_expect_tx(&mbar[slot ^ 1], bytes);
-            tma_load_1d(wbase + (slot ^ 1) * bufb, a.src + nb * a.ld, bytes, &mbar[slot ^ 1]);
-        }
-        if (XL && !XB) {
-            cp_async_wait();
-            __syncwarp();
-        } else {
-            mbar_wait(&mbar[slot], NBUF == 2 ? ((it >> 1) & 1) : (it & 1));
-        }
-        double *M = reinterpret_cast<double *>(wbase + slot * bufb);
+        mbar_wait(&mbar[0], it & 1);
+        double *M = reinterpret_cast<double *>(wbase);
 
         int poff[CPL], p[CPL];
         double v[CPL], ucol[CPL];
         int steps = 0;
-        if (XB) {  // column c -> its location's slot (lanes without a column: slot of location j)
-            const int j = (ijkl >> 8) & 0xff, l = ijkl >> 24;
-            cofs[0] = col0 < m ? x_col(col0, j, l) : j;
-        }
         if constexpr (CPL == 1) {
-            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M + cofs[0], m, ldm, lane, poff[0], v[0], ucol[0], steps);
-            else warp_lap_solve1<false>(M + cofs[0], m, ldm, lane, poff[0], v[0], ucol[0], steps);
+            if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M, m, lane, scratch, poff[0], v[0], ucol[0], steps);
+            else warp_lap_solve1<false>(M, m, lane, scratch, poff[0], v[0], ucol[0], steps);
         } else {
-            if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M + lane, m, lane, poff, v, ucol, steps);
-            else warp_lap_solve<CPL, false>(M + lane, m, lane, poff, v, ucol, steps);
+            if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M, m, lane, scratch, poff, v, ucol, steps);
+            else warp_lap_solve<CPL, false>(M, m, lane, scratch, poff, v, ucol, steps);
         }
         bool bad;
-        double S;
-        unsigned nijkl = 0;
-        int inext = icur;
-        if (XB) {
-            const double *X = a.X;
-            S = warp_lap_epilogue<CPL>(
-                M,
-                [&](int r, int t, int c) {
-                    const double *src = X + (size_t)x_pick<CPL>(xr, r) * (size_t)a.g.np + cofs[t];
-                    return c < m ? *src : 0.0;
-                },
-                m, ldm, cofs, lane, col0, poff, p, v, ucol, xurow, xsel, ldm, bad);
-            // residual rows back to their runs (scatter4; rows >= m: junk row 0), then the
-            // next block's rows into the buffer once the stores have read it
-            x_rows4<false>(&xrow, M, ldm, m4, xr[0], lane, &mbar[0]);
-            if (lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            if (nb < a.count) {
-                inext = icur;
-                nijkl = decode_l2(a, nb, inext);
-                x_rows<CPL>(a.g, nijkl, m, lane, xr);
-                if (lane == 0) {
-                    bulk_wait_read();
-                    mbar_expect_tx(&mbar[0], (uint32_t)(m4 * ldm * 8));
-                }
-                x_rows4<true>(&xrow, M, ldm, m4, xr[0], lane, &mbar[0]);
-            }
-        } else if (XL) {
-            XCols<CPL> xc;
-            x_cols<CPL>(a.X, M, ijkl, m, col0, xc);
-            const int np = a.g.np;
-            S = warp_lap_epilogue<CPL>(
-                M,
-                [&](int r, int t, int c) {
-                    const double *src = xc.g[t] + (size_t)x_pick<CPL>(xr, r) * (size_t)np;
-                    return c < m ? *src : 0.0;
-                },
-                m, m, cofs, lane, col0, poff, p, v, ucol, urow, sel, 1, bad);
-            // residual rows back to their runs, then the next block's rows into the buffer
-            x_store<CPL>(np, m, xr, xc);
-            __syncwarp();
-            if (nb < a.count) {
-                inext = icur;
-                nijkl = decode_l2(a, nb, inext);
-                x_rows<CPL>(a.g, nijkl, m, lane, xr);
-                x_cols<CPL>(a.X, M, nijkl, m, col0, xc);
-                x_load<CPL>(np, m, xr, xc);
-            }
-        } else {
-            const double *Mg = a.src + b * a.ld;
-            S = warp_lap_epilogue<CPL>(
-                M, [&](int r, int t, int c) { return c < m ? Mg[r * m + c] : 0.0; }, m, m, cofs, lane, col0, poff, p,
-                v, ucol, urow, sel, 1, bad);
-        }
+        const double *Mg = a.src + b * a.ld;
+        const double S = warp_lap_epilogue<CPL>(
+            M, [&](int r, int t, int c) { return c < m ? Mg[r * m + c] : 0.0; }, m, m, cofs, lane, col0, poff, p, v,
+            ucol, urow, sel, 1, bad);
         anybad |= bad;
-        if (!XL && lane == 0) {
+        if (lane == 0) {
             tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global
-            if (NBUF == 1 && nb < a.count) {          // buffer free once the store has read it
-                if (WAIT) wait_transfer(a, facility_of(a.g, nb, hint_load), ready);
+            if (nb < a.count) {                       // buffer free once the store has read it
                 bulk_wait_read();
                 mbar_expect_tx(&mbar[0], bytes);
                 tma_load_1d(wbase, a.src + nb * a.ld, bytes, &mbar[0]);
@@ -924,7 +738,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_cons
                 }
                 const Geom &g = a.g;
                 const int n = g.n, n1 = n - 1;
-                const unsigned q = XL ? ijkl : decode_l2(a, b, icur);
+                const unsigned q = decode_l2(a, b, icur);
                 const int i = q & 0xff, j = (q >> 8) & 0xff, k = (q >> 16) & 0xff, l = q >> 24;
                 // C was spread to D and zeroed: c <- 0 + S = S.
                 a.C[(int64_t)(i * n + j) * g.ldc + (k - 1) * n1 + (l - (l > j))] = S;
@@ -986,10 +800,6 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a, const __grid_cons
             }
         }
         __syncwarp();
-        if (XL) {
-            ijkl = nijkl;
-            icur = inext;
-        }
         b = nb;
     }
     if (lane == 0) bulk_wait_all();
@@ -1179,13 +989,7 @@ __global__ void k_sigma(const Geom g, const double *__restrict__ B, const double
                         double *__restrict__ sigma, const Ctl *ctl, Sched *sched)
 {
     if (ctl->stopped) return;
-    if (blockIdx.x == 0 && threadIdx.x < kMaxN) {
-        sched->done[threadIdx.x] = 0;
-        if (threadIdx.x == 0) {
-            sched->head = 0;
-            sched->thead = 0;
-        }
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) sched->head = 0;
     const int n = g.n, n1 = n - 1;
     const int64_t n4 = (int64_t)n * n * n * n;
     const double div1 = (double)(n - 1), div2 = (double)(2 * (n - 2));
@@ -1358,14 +1162,6 @@ __global__ void __launch_bounds__(256, 6) k_transfer(const TransferArgs A)
         for (int vw = 0; vw < 3; vw++)
             if (addr[h][vw] != NOIDX) A.D[vbs(vw) * ld2 + addr[h][vw]] = sv[vw][tix(x, y, z)];
     }
-    if (A.publish) {  // overlapped mode: this tile of facility i is final (release)
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            atomicAdd(&A.sched->done[i], 1u);
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1519,124 +1315,6 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 8 : 11) k_transfer_tma(const T
             if (base != NOIDX && f < n && f != a && f != b)
                 D2[base + (unsigned)(f - (f > a) - (f > b))] =
                     INBOX ? box[2][box_pos<BX0>(2, f, a, b, j0, l0, q0, o2)] : mean[z * MA + x * MB + y];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// Class layout X.  The stored value of class member e of class
-// {(a,x),(b,y),(c,z)}, a < b < c (reading R11/R12), lives in section r of X,
-// where r is the position of the member's ROW facility in the sorted triple:
-//   r = 0: e1, block D{ax,by}, row c  ->  X[0][t][x][y][z]
-//   r = 1: e2, block D{ax,cz}, row b  ->  X[1][t][x][z][y]
-//   r = 2: e3, block D{by,cz}, row a  ->  X[2][t][y][z][x]
-// t = lexicographic index of (a,b,c).  In every section the index is
-// [t][block's first location][block's second location][row facility's location], so row p
-// of block D{ij,kl} is the contiguous run X[r][t][j][l][0..n) (columns q != j, l used):
-// the level-2 LAP reads and writes whole rows, and the transfer moves whole 8x8x8 boxes of
-// each section by tensor-map TMA (no skip-indexed windows, no overlap between tiles).
-// Slots with repeated locations belong to no class and are never read.
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ void tma_store_4d(const void *tmap, int c0, int c1, int c2, int c3, const void *src)
-{
-    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                     reinterpret_cast<uint64_t>(tmap)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
-                 : "memory");
-}
-
-// k_transfer_x — spreading C->D fused with the transfer between the 3 members of every class
-// (reading R10/R11), in the class layout: one CTA per facility triple
-// t = (a,b,c) x 8x8x8 tile of locations (x,y,z).  The three sections' boxes are loaded by
-// TMA, every thread forms the mean of 2 classes with the oracle's operation order
-//   mu = ((e1 + sigma1) + (e2 + sigma2)) + (e3 + sigma3)) / 3,
-// writes it over the three member slots in shared memory, and the boxes are stored back by
-// TMA (out-of-range box parts are zero-filled on load and clipped on store).
-constexpr int kXT = 128;  // k_transfer_x threads per CTA (16 CTAs per SM: more tiles in flight)
-__global__ void __launch_bounds__(kXT, 16) k_transfer_x(const TransferArgs A, const __grid_constant__ CUtensorMap xm)
-{
-    if (A.ctl->stopped) return;
-    __shared__ __align__(128) double box[3][TT * TT * TT];
-    __shared__ double rsig[3][TT * TT];
-    __shared__ __align__(8) uint64_t mbar;
-    const Geom &g = A.g;
-    const int n = g.n, n1 = n - 1, ntile = A.ntile;
-    const int t = (int)blockIdx.z, tri = A.triples[t];
-    const int fa = tri & 0xff, fb = (tri >> 8) & 0xff, fc = tri >> 16;
-    const int tx = (int)((blockIdx.y * A.ntile_mul) >> 16), ty = (int)blockIdx.y - tx * ntile;
-    const int x0 = tx * TT, y0 = ty * TT, z0 = (int)blockIdx.x * TT;
-    const int tid = threadIdx.x;
-    const bool dz = A.d_zero != 0;
-    if (tid == 0 && !dz) {
-        mbar_init(&mbar, 1);
-        fence_mbar_init();
-        mbar_expect_tx(&mbar, 3u * TT * TT * TT * 8u);
-        tma_load_4d(box[0], &xm, z0, y0, x0, t, &mbar);              // [x][y][z]
-        tma_load_4d(box[1], &xm, y0, z0, x0, g.ntri + t, &mbar);     // [x][z][y]
-        tma_load_4d(box[2], &xm, x0, z0, y0, 2 * g.ntri + t, &mbar); // [y][z][x]
-    }
-    // sigma of each member's block (k_sigma): member 1 by (x,y), 2 by (x,z), 3 by (y,z)
-    for (int e = tid; e < 3 * TT * TT; e += kXT) {
-        const int vw = e >> 6, u = x0 * (vw < 2) + y0 * (vw == 2) + ((e >> 3) & 7),
-                  w = (vw == 0 ? y0 : z0) + (e & 7);
-        const int f = vw == 2 ? fb : fa, h = vw == 0 ? fb : fc;
-        double sg = 0.0;
-        if (u < n && w < n && u != w)
-            sg = A.sigma[(unsigned)g.off[f] + (unsigned)(u * (n1 - f) * n1 + (h - f - 1) * n1 + (w - (w > u)))];
-        rsig[vw][e & 63] = sg;
-    }
-    __syncthreads();
-    if (!dz) mbar_wait(&mbar, 0);
-#pragma unroll
-    for (int hh = 0; hh < TT * TT * TT / kXT; hh++) {
-        const int e = tid + kXT * hh;
-        const int u = e >> 6, v = (e >> 3) & 7, w = e & 7;
-        const int x = x0 + u, y = y0 + v, z = z0 + w;
-        if (x < n && y < n && z < n && x != y && x != z && y != z) {
-            const int p0 = (u * TT + v) * TT + w, p1 = (u * TT + w) * TT + v, p2 = (v * TT + w) * TT + u;
-            const double e1 = (dz ? 0.0 : box[0][p0]) + rsig[0][u * TT + v];
-            const double e2 = (dz ? 0.0 : box[1][p1]) + rsig[1][u * TT + w];
-            const double e3 = (dz ? 0.0 : box[2][p2]) + rsig[2][v * TT + w];
-            const double mu = div3((e1 + e2) + e3);
-            box[0][p0] = mu;
-            box[1][p1] = mu;
-            box[2][p2] = mu;
-        }
-    }
-    fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA stores
-    __syncthreads();
-    if (tid == 0) {
-        tma_store_4d(&xm, z0, y0, x0, t, box[0]);
-        tma_store_4d(&xm, y0, z0, x0, g.ntri + t, box[1]);
-        tma_store_4d(&xm, x0, z0, y0, 2 * g.ntri + t, box[2]);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        bulk_wait_read();  // shared memory stays valid until the stores have read it
-    }
-}
-
-// stored blocks <-> class layout (export, warm folds, A/B with the block path): one warp per
-// stored block, lanes over columns, rows streamed; valid entries only.
-__global__ void __launch_bounds__(256) k_xconv(const Geom g, double *__restrict__ D, double *__restrict__ X, int to_x)
-{
-    const int n = g.n, n1 = n - 1, m = n - 2, lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    int hint = 0;
-    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < g.nblk; b += nw) {
-        while (hint + 1 < n && b >= g.off[hint + 1]) hint++;
-        while (hint > 0 && b < g.off[hint]) hint--;
-        const int i = hint;
-        int rem = (int)(b - g.off[i]);
-        const int per_j = (n1 - i) * n1, j = rem / per_j;
-        rem -= j * per_j;
-        const int k = i + 1 + rem / n1, li = rem % n1, l = li + (li >= j);
-        double *blk = D + b * g.ld2;
-        for (int r = 0; r < m; r++) {
-            const size_t row = (size_t)x_row(g, i, j, k, l, x_rowfac(r, i, k)) * (size_t)g.np;
-            for (int c = lane; c < m; c += 32) {
-                double *xs = X + row + x_col(c, j, l);
-                if (to_x) *xs = blk[r * m + c];
-                else blk[r * m + c] = *xs;
-            }
         }
     }
 }
@@ -1796,308 +1474,6 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
     return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------------------
-// k_fused_x — the transfer and the level-2 concentration of
-// one iteration in ONE persistent kernel over the class layout, so that the HBM-bound
-// transfer runs on the same SMs as the issue-bound LAPs instead of before them.  Every warp
-// is a worker with one 7 KB shared-memory buffer and takes either
-//   * a transfer tile: facility triple t x 4x8x8 locations — three TMA boxes, 8 class means
-//     per lane (the operation order of k_transfer_x), three TMA box stores, then the tile
-//     is published in done[smallest facility] (release), or
-//   * a level-2 LAP of a stored block D{ij,kl} (as k_lap<1,1,0,1>), once every triple with
-//     smallest facility <= min(i, n-3) is published: those are exactly the triples with a
-//     member in the block, and no later tile touches it (so the LAP may overwrite it).
-// Queues are in facility order.  One warp in four prefers transfer tiles; the others take
-// LAPs whenever the next one is ready and transfer tiles otherwise, so the transfer runs at
-// full width at the start of the iteration and whenever the LAPs catch up with it.  Transfer
-// tiles never wait: the kernel cannot deadlock.  The results are bit-identical to
-// k_transfer_x followed by k_lap (the same operations on the same values).
-// ---------------------------------------------------------------------------------------
-struct FusedArgs {
-    LapArgs L;
-    TransferArgs T;
-    int ntx, nyz;          // tiles: ceil(n / 4) x-tiles, ceil(n / 8) y- and z-tiles
-    int tpt;               // tiles per facility triple
-    long long ntiles;      // all transfer tiles
-    int wbytes;            // shared memory per warp buffer
-    int tmask;             // warps with (warp & tmask) == 0 prefer transfer tiles
-};
-constexpr int kFusedTileX = 4;
-__device__ __forceinline__ void fused_transfer_tile(const FusedArgs &F, long long job, double *buf, uint64_t *mbar,
-                                                    uint32_t &phase, int lane, const CUtensorMap *xa,
-                                                    const CUtensorMap *xb)
-{
-    const TransferArgs &A = F.T;
-    const Geom &g = A.g;
-    const int n = g.n, n1 = n - 1;
-    const int t = (int)(job / F.tpt);
-    int rem = (int)(job - (long long)t * F.tpt);
-    const int nyz2 = F.nyz * F.nyz;
-    const int tx = rem / nyz2;
-    rem -= tx * nyz2;
-    const int ty = rem / F.nyz, tz = rem - ty * F.nyz;
-    const int x0 = tx * kFusedTileX, y0 = ty * TT, z0 = tz * TT;
-    const int tri = A.triples[t];
-    const int fa = tri & 0xff, fb = (tri >> 8) & 0xff, fc = tri >> 16;
-    double *b0 = buf, *b1 = buf + 256, *b2 = buf + 512, *sig = buf + 768;
-    const bool dz = A.d_zero != 0;
-    if (lane == 0 && !dz) {
-        mbar_expect_tx(mbar, 3u * 256u * 8u);
-        tma_load_4d(b0, xa, z0, y0, x0, t, mbar);               // [x:4][y:8][z:8]
-        tma_load_4d(b1, xa, y0, z0, x0, g.ntri + t, mbar);      // [x:4][z:8][y:8]
-        tma_load_4d(b2, xb, x0, z0, y0, 2 * g.ntri + t, mbar);  // [y:8][z:8][x:4]
-    }
-    // sigma of the members' blocks: (x,y) 32, (x,z) 32, (y,z) 64
-#pragma unroll
-    for (int h = 0; h < 4; h++) {
-        const int e = lane + 32 * h;
-        int vw, u, w;
-        if (e < 32) { vw = 0; u = x0 + (e >> 3); w = y0 + (e & 7); }
-        else if (e < 64) { vw = 1; u = x0 + ((e - 32) >> 3); w = z0 + (e & 7); }
-        else { vw = 2; u = y0 + ((e - 64) >> 3); w = z0 + (e & 7); }
-        const int f = vw == 2 ? fb : fa, hh = vw == 0 ? fb : fc;
-        double sg = 0.0;
-        if (u < n && w < n && u != w)
-            sg = A.sigma[(unsigned)g.off[f] + (unsigned)(u * (n1 - f) * n1 + (hh - f - 1) * n1 + (w - (w > u)))];
-        sig[e] = sg;
-    }
-    __syncwarp();
-    if (!dz) {
-        mbar_wait(mbar, phase);
-        phase ^= 1;
-    }
-#pragma unroll
-    for (int h = 0; h < 8; h++) {
-        const int e = lane + 32 * h;
-        const int u = e >> 6, v = (e >> 3) & 7, w = e & 7;
-        const int x = x0 + u, y = y0 + v, z = z0 + w;
-        if (x < n && y < n && z < n && x != y && x != z && y != z) {
-            const int p0 = (u * TT + v) * TT + w, p1 = (u * TT + w) * TT + v, p2 = (v * TT + w) * kFusedTileX + u;
-            const double e1 = (dz ? 0.0 : b0[p0]) + sig[u * TT + v];
-            const double e2 = (dz ? 0.0 : b1[p1]) + sig[32 + u * TT + w];
-            const double e3 = (dz ? 0.0 : b2[p2]) + sig[64 + v * TT + w];
-            const double mu = div3((e1 + e2) + e3);
-            b0[p0] = mu;
-            b1[p1] = mu;
-            b2[p2] = mu;
-        }
-    }
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-        tma_store_4d(xa, z0, y0, x0, t, b0);
-        tma_store_4d(xa, y0, z0, x0, g.ntri + t, b1);
-        tma_store_4d(xb, x0, z0, y0, 2 * g.ntri + t, b2);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        bulk_wait_all();  // written (not only read): the tile is published below
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        atomicAdd(&A.sched->done[fa], 1u);
-    }
-    __syncwarp();
-}
-
-__global__ void __launch_bounds__(1024, 1) k_fused_x(const FusedArgs F, const __grid_constant__ CUtensorMap xrow,
-                                                     const __grid_constant__ CUtensorMap xa,
-                                                     const __grid_constant__ CUtensorMap xb)
-{
-    const LapArgs &a = F.L;
-    if (__shfl_sync(FULL_MASK, a.ctl->stopped, 0)) return;
-    extern __shared__ __align__(128) unsigned char smem[];  // buffers at 1 KB multiples: boxes 128-byte aligned
-    const int wpc = blockDim.x >> 5, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0),
-              lane = threadIdx.x & 31;
-    const int col0 = 31 - lane;
-    const Geom &g = a.g;
-    const int n = g.n, m = a.m, m4 = (m + 3) & ~3, ldm = (n + 5) & ~3, np = g.np;
-    double *const buf = reinterpret_cast<double *>(smem + (size_t)warp * F.wbytes);
-    uint64_t *const mbar = reinterpret_cast<uint64_t *>(smem + (size_t)wpc * F.wbytes + (size_t)warp * 16);
-    double *const xurow = buf + n, *const xsel = xurow + 1;
-    Sched *const sc = a.sched;
-    if (lane == 0) {
-        mbar_init(mbar, 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    uint32_t phase = 0;
-    int ready = -1;  // every triple with smallest facility <= ready is published
-    int icur = 0;
-    long long lb = 0, lend = 0, tb = 0, tend = 0;
-    bool t_out = false, l_out = false, anybad = false;
-    const bool prefer_t = (warp & F.tmask) == 0;
-    const long long CH = 4;
-    // lane 0 polls the published counters; the result is broadcast
-    auto is_ready = [&](int f) -> bool {
-        const int need = f < n - 3 ? f : n - 3;
-        int r = ready;
-        if (lane == 0) {
-            while (r < need) {
-                const int x = r + 1;
-                const unsigned total = (unsigned)F.tpt * (unsigned)((n - 1 - x) * (n - 2 - x) / 2);
-                if (ld_acquire(&sc->done[x]) >= total) r++;
-                else break;
-            }
-        }
-        ready = __shfl_sync(FULL_MASK, r, 0);
-        return ready >= need;
-    };
-    auto grab_l = [&]() {
-        long long c0 = 0;
-        if (lane == 0) c0 = (long long)atomicAdd(&sc->head, (unsigned long long)CH);
-        lb = __shfl_sync(FULL_MASK, c0, 0);
-        lend = lb + CH < a.count ? lb + CH : a.count;
-        if (lb >= a.count) l_out = true;
-    };
-    auto grab_t = [&]() {
-        long long c0 = 0;
-        if (lane == 0) c0 = (long long)atomicAdd(&sc->thead, (unsigned long long)CH);
-        tb = __shfl_sync(FULL_MASK, c0, 0);
-        tend = tb + CH < F.ntiles ? tb + CH : F.ntiles;
-        if (tb >= F.ntiles) t_out = true;
-    };
-    auto lap_job = [&](long long b) {
-        const unsigned ijkl = decode_l2(a, b, icur);
-        unsigned xr[1];
-        x_rows<1>(g, ijkl, m, lane, xr);
-        if (lane == 0) {
-            fence_proxy_async_global();  // published generic-side order -> our TMA reads
-            mbar_expect_tx(mbar, (uint32_t)(m4 * ldm * 8));
-        }
-        x_rows4<true>(&xrow, buf, ldm, m4, xr[0], lane, mbar);
-        mbar_wait(mbar, phase);
-        phase ^= 1;
-        const int j = (ijkl >> 8) & 0xff, l = ijkl >> 24;
-        int cofs[1] = {col0 < m ? x_col(col0, j, l) : j};
-        int poff[1], p[1], steps = 0;
-        double v[1], ucol[1];
-        warp_lap_solve1<false>(buf + cofs[0], m, ldm, lane, poff[0], v[0], ucol[0], steps);
-        bool bad;
-        const double *X = a.X;
-        const double S = warp_lap_epilogue<1>(
-            buf,
-            [&](int r, int t, int c) {
-                const double *src = X + (size_t)x_pick<1>(xr, r) * (size_t)np + cofs[t];
-                return c < m ? *src : 0.0;
-            },
-            m, ldm, cofs, lane, col0, poff, p, v, ucol, xurow, xsel, ldm, bad);
-        anybad |= bad;
-        x_rows4<false>(&xrow, buf, ldm, m4, xr[0], lane, mbar);
-        if (lane == 0) {
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            const int i = ijkl & 0xff, k = (ijkl >> 16) & 0xff, n1 = n - 1;
-            a.C[(int64_t)(i * n + j) * g.ldc + (k - 1) * n1 + (l - (l > j))] = S;  // reading R12
-            a.C[(int64_t)(k * n + l) * g.ldc + i * n1 + (j - (j > l))] = S;
-            bulk_wait_read();  // the buffer is free once the stores have read it
-        }
-        __syncwarp();
-    };
-    for (;;) {
-        if (tb < tend) {  // tiles already taken are finished first (others may wait on them)
-            fused_transfer_tile(F, tb++, buf, mbar, phase, lane, &xa, &xb);
-            continue;
-        }
-        if (!(prefer_t && !t_out)) {  // LAP first (one warp in four: transfer first)
-            if (lb >= lend && !l_out) grab_l();
-            if (lb < lend && is_ready(facility_of(g, lb, icur))) {
-                lap_job(lb++);
-                continue;
-            }
-        }
-        if (!t_out) {
-            grab_t();
-            if (tb < tend) continue;
-        }
-        // no transfer tile left: LAPs only (waiting for the tiles still in flight)
-        if (lb >= lend && !l_out) grab_l();
-        if (lb >= lend) break;
-        unsigned spins = 0;
-        while (!is_ready(facility_of(g, lb, icur))) {
-            __nanosleep(256);
-            if (++spins > (1u << 26)) __trap();  // ~20 s without progress: fail, never hang
-        }
-        lap_job(lb++);
-    }
-    if (lane == 0) bulk_wait_all();
-    if (anybad && lane == 0) atomicOr(&a.ctl->err, 1);
-}
-
-cudaError_t launch_fused_x(const Geom &g, const TransferArgs &A, double *X, double *C, Ctl *ctl, Sched *sched,
-                           int num_sms, const CUtensorMap &xa, const CUtensorMap &xb, const CUtensorMap &xrow,
-                           cudaStream_t st)
-{
-    const int n = g.n, m = n - 2;
-    if (m > 32 || n < kXMin) return cudaErrorInvalidValue;
-    FusedArgs F{};
-    LapArgs &a = F.L;
-    a.lvl = LAP_L2;
-    a.g = g;
-    a.m = m;
-    a.count = g.nblk;
-    a.ld = g.ld2;
-    a.C = C;
-    a.ctl = ctl;
-    a.X = X;
-    a.sched = sched;
-    a.mag_n1 = (uint32_t)((0x100000000ull + (uint64_t)(n - 2)) / (uint64_t)(n - 1));
-    for (int i = 0; i + 1 < n; i++) {
-        const uint64_t d = (uint64_t)(n - 1 - i) * (uint64_t)(n - 1);
-        a.mag_pj[i] = (uint32_t)((0x100000000ull + d - 1) / d);
-    }
-    F.T = A;
-    F.ntx = (n + kFusedTileX - 1) / kFusedTileX;
-    F.nyz = (n + TT - 1) / TT;
-    F.tpt = F.ntx * F.nyz * F.nyz;
-    F.ntiles = (long long)F.tpt * g.ntri;
-    const int ldm = (n + 5) & ~3;
-    size_t lapb = (size_t)((m + 3) & ~3) * ldm * 8;
-    size_t wb = lapb > 7168 ? lapb : 7168;  // a transfer tile needs 3 x 2 KB boxes + 1 KB sigma
-    wb = (wb + 1023) & ~size_t(1023);
-    F.wbytes = (int)wb;
-    F.tmask = 3;  // one warp in four prefers transfer tiles (QAP_FUSED_TMASK: experiment knob)
-    if (const char *ev = getenv("QAP_FUSED_TMASK")) F.tmask = atoi(ev);
-    int wpc = 32;
-    while (wpc > 1 && (wb + 16) * wpc > (size_t)226 * 1024) wpc--;
-    const size_t smem = (wb + 16) * wpc;
-    static std::mutex mu;
-    static uint64_t done_dev = 0;
-    {
-        int dev = 0;
-        cudaError_t e0 = cudaGetDevice(&dev);
-        if (e0 != cudaSuccess) return e0;
-        std::lock_guard<std::mutex> lk(mu);
-        if (dev >= 64 || !((done_dev >> dev) & 1)) {
-            int mx = 0;
-            if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
-                return e0;
-            if ((e0 = cudaFuncSetAttribute(k_fused_x, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
-                cudaSuccess)
-                return e0;
-            if (dev < 64) done_dev |= 1ull << dev;
-        }
-    }
-    k_fused_x<<<num_sms, 32 * wpc, smem, st>>>(F, xrow, xa, xb);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_transfer_x(const TransferArgs &A, const CUtensorMap &xmap, cudaStream_t st)
-{
-    const int n = A.g.n;
-    if (A.ntile > 8 || A.g.ntri > 65535) return cudaErrorInvalidValue;  // n <= kMaxN = 64
-    TransferArgs B = A;
-    B.ntile_mul = (65536u + (unsigned)A.ntile - 1u) / (unsigned)A.ntile;
-    dim3 grid(A.ntile, A.ntile * A.ntile, A.g.ntri);
-    (void)n;
-    k_transfer_x<<<grid, kXT, 0, st>>>(B, xmap);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_xconv(const Geom &g, double *D, double *X, int to_x, int num_sms, cudaStream_t st)
-{
-    int64_t blocks = (g.nblk + 7) / 8;
-    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
-    k_xconv<<<(int)blocks, 256, 0, st>>>(g, D, X, to_x);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_transfer(const TransferArgs &A, int ntiles_list, cudaStream_t st)
 {
     const int n = A.g.n;
@@ -2125,10 +1501,10 @@ cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, do
     return cudaGetLastError();
 }
 
-template <int CPL, int NBUF, bool WAIT, bool XL = false>
+template <int CPL>
 static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
 {
-    const size_t smem = lap_warp_smem(a.m, CPL, NBUF, (XL && CPL == 1) ? ((a.g.n + 5) & ~3) : 0) * wpc;
+    const size_t smem = lap_warp_smem(a.m, CPL) * wpc;
     // The dynamic-smem limit is a process-wide attribute of the kernel: raise it once per
     // device to the opt-in maximum (setting it per launch to the exact size would race
     // between threads launching different sizes, e.g. concurrent B&B workers).
@@ -2143,8 +1519,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
             int mx = 0;
             if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
                 return e0;
-            if ((e0 = cudaFuncSetAttribute(k_lap<CPL, NBUF, WAIT, XL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) !=
-                cudaSuccess)
+            if ((e0 = cudaFuncSetAttribute(k_lap<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) != cudaSuccess)
                 return e0;
             if (dev < 64) done_dev |= 1ull << dev;
         }
@@ -2152,7 +1527,7 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     if (smem > 232448) return cudaErrorInvalidValue;
     cudaError_t e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL, NBUF, WAIT, XL>, 32 * wpc, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL>, 32 * wpc, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int64_t want = (a.count + wpc - 1) / wpc;
@@ -2164,28 +1539,22 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     LapArgs b = a;
     const int64_t warps = (int64_t)grid * wpc;
     b.chunk = a.count >= 8 * warps ? 4 : (a.count >= 3 * warps ? 2 : 1);
-    CUtensorMap xm{};
-    if (XL && CPL == 1) {
-        if (!a.xrow) return cudaErrorInvalidValue;
-        xm = *a.xrow;
-    }
-    k_lap<CPL, NBUF, WAIT, XL><<<grid, 32 * wpc, smem, st>>>(b, xm);
+    k_lap<CPL><<<grid, 32 * wpc, smem, st>>>(b);
     return cudaGetLastError();
 }
 
-// lap_cfg: bits 0-7 = warps per CTA (0: default), bit 8 = double buffering,
-// bits 12-15 = CTAs per SM in dynamic (overlapped) mode (0: 1).
+// lap_cfg: bits 0-7 = warps per CTA (0: default), bits 12-15 = CTAs per SM in dynamic mode
+// (0: 1).
 static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cudaStream_t st)
 {
     const int cpl = a.m <= 32 ? 1 : 2;
     if (a.m > 64) return cudaErrorInvalidValue;
-    const int nbuf = (lap_cfg & 0x100) ? 2 : 1;
     int wpc = lap_cfg & 0xff;
     int cps = (lap_cfg >> 12) & 0xf;
-    if (wpc <= 0 && a.sched && !a.X && a.ntile3 == 0) {
+    if (wpc <= 0 && a.sched) {
         // default level-2 configuration: the most resident warps per SM that shared memory
         // allows (228 KB per SM, 1 KB reserved per CTA), e.g. 2 CTAs x 17 warps at m = 28
-        const size_t ws = lap_warp_smem(a.m, cpl, nbuf);
+        const size_t ws = lap_warp_smem(a.m, cpl);
         int best = 0;
         for (int c = 1; c <= 2; c++)
             for (int w = 32; w >= 1; w--)
@@ -2198,30 +1567,12 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
     if (wpc <= 0) wpc = a.sched ? 32 : 8;
     if (cps <= 0) cps = 1;
     const size_t cap = a.sched ? (size_t)233472 / cps - 1024 : (size_t)226 * 1024;
-    const int ldrow = (a.X && cpl == 1) ? ((a.g.n + 5) & ~3) : 0;
-    while (wpc > 1 && lap_warp_smem(a.m, cpl, nbuf, ldrow) * wpc > cap) wpc--;
-    if (a.X) {  // class layout (no overlap mode, single buffer)
-        if (a.sched && a.ntile3 > 0) return cudaErrorInvalidValue;
-        return cpl == 1 ? launch_lap_on<1, 1, false, true>(a, num_sms, wpc, cps, st)
-                        : launch_lap_on<2, 1, false, true>(a, num_sms, wpc, cps, st);
-    }
-    if (a.sched && a.ntile3 > 0) {  // overlapped with the transfer: blocks wait for their facility
-        if (cpl == 1)
-            return nbuf == 2 ? launch_lap_on<1, 2, true>(a, num_sms, wpc, cps, st)
-                             : launch_lap_on<1, 1, true>(a, num_sms, wpc, cps, st);
-        return nbuf == 2 ? launch_lap_on<2, 2, true>(a, num_sms, wpc, cps, st)
-                         : launch_lap_on<2, 1, true>(a, num_sms, wpc, cps, st);
-    }
-    if (cpl == 1)
-        return nbuf == 2 ? launch_lap_on<1, 2, false>(a, num_sms, wpc, cps, st)
-                         : launch_lap_on<1, 1, false>(a, num_sms, wpc, cps, st);
-    return nbuf == 2 ? launch_lap_on<2, 2, false>(a, num_sms, wpc, cps, st)
-                     : launch_lap_on<2, 1, false>(a, num_sms, wpc, cps, st);
+    while (wpc > 1 && lap_warp_smem(a.m, cpl) * wpc > cap) wpc--;
+    return cpl == 1 ? launch_lap_on<1>(a, num_sms, wpc, cps, st) : launch_lap_on<2>(a, num_sms, wpc, cps, st);
 }
 
 cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, double *B, Ctl *ctl,
-                             double *trace, int num_sms, int lap_warps, Sched *sched, int wait, cudaStream_t st,
-                             double *X, const CUtensorMap *xrow)
+                             double *trace, int num_sms, int lap_warps, Sched *sched, cudaStream_t st)
 {
     LapArgs a{};
     a.lvl = lvl;
@@ -2235,8 +1586,6 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
     switch (lvl) {
     case LAP_L2:
         a.m = n - 2; a.count = g.nblk; a.ld = g.ld2; a.src = D; a.dst = D;
-        a.X = X;
-        a.xrow = xrow;
         wpc = lap_warps;
         a.mag_n1 = (uint32_t)((0x100000000ull + (uint64_t)(n - 2)) / (uint64_t)(n - 1));
         for (int i = 0; i + 1 < n; i++) {
@@ -2244,10 +1593,6 @@ cudaError_t launch_lap_level(LapLevel lvl, const Geom &g, double *D, double *C, 
             a.mag_pj[i] = (uint32_t)((0x100000000ull + d - 1) / d);
         }
         a.sched = sched;
-        {
-            const int nt = (n + TT - 1) / TT;
-            a.ntile3 = wait ? nt * nt * nt : 0;  // 0: the transfer already completed (no waits)
-        }
         break;
     case LAP_L1_ACC:
     case LAP_L1_SET:
@@ -2278,8 +1623,7 @@ cudaError_t launch_lap_l2_local(const Geom &g, double *Dloc, int64_t count, doub
     a.src = Dloc;
     a.dst = Dloc;
     a.bo.S = Sout;
-    a.sched = sched;  // dynamic queue (reset by k_sigma), no transfer waits
-    a.ntile3 = 0;
+    a.sched = sched;  // dynamic queue (reset by k_sigma)
     return dispatch_lap(a, num_sms, lap_cfg, st);
 }
 

@@ -13,6 +13,83 @@
 
 namespace rlt2 {
 
+namespace {
+// Host-staged collectives (qap_host_transport): pinned staging buffers grown on demand; the
+// stream is drained before each callback and after the copies back.
+struct HostTransport : Transport {
+    qap_host_transport cb{};
+    int world = 1, rank = 0;
+    double *hsend = nullptr, *hrecv = nullptr;
+    size_t cap = 0;
+    std::vector<int64_t> off, cnt;
+    std::string err;
+    ~HostTransport() override
+    {
+        cudaFreeHost(hsend);
+        cudaFreeHost(hrecv);
+    }
+    cudaError_t grow(size_t n)
+    {
+        if (n <= cap) return cudaSuccess;
+        cudaFreeHost(hsend);
+        cudaFreeHost(hrecv);
+        hsend = hrecv = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void **>(&hsend), n * 8);
+        if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void **>(&hrecv), n * 8);
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+    cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, cudaStream_t st) override
+    {
+        const size_t tot = (size_t)P.total_slots * kSlot;
+        if (tot == 0) return cudaSuccess;
+        cudaError_t e = grow(tot);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hsend, send, tot * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        off.assign(P.G, 0);
+        cnt.assign(P.G, 0);
+        for (int q = 0; q < P.G; q++) {
+            if (q == P.r) continue;
+            off[q] = P.peer_off[q] * kSlot;
+            cnt[q] = P.peer_slots[q] * kSlot;
+        }
+        if (cb.exchange(cb.ctx, hsend, hrecv, off.data(), cnt.data(), world, rank) != 0) {
+            err = "host transport: exchange callback failed";
+            return cudaErrorUnknown;
+        }
+        if ((e = cudaMemcpyAsync(recv, hrecv, tot * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+        return cudaStreamSynchronize(st);
+    }
+    cudaError_t allgather(const ShardPlan &P, double *S_all, cudaStream_t st) override
+    {
+        const size_t tot = (size_t)P.blk_lo[P.G];
+        if (tot == 0) return cudaSuccess;
+        cudaError_t e = grow(tot);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hrecv, S_all, tot * 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        if (cb.allgather(cb.ctx, hrecv, P.blk_lo.data(), world, rank) != 0) {
+            err = "host transport: allgather callback failed";
+            return cudaErrorUnknown;
+        }
+        if ((e = cudaMemcpyAsync(S_all, hrecv, tot * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+        return cudaStreamSynchronize(st);
+    }
+    const char *error() const override { return err.c_str(); }
+};
+}  // namespace
+
+Transport *make_host_transport(const qap_host_transport &cb, int world, int rank)
+{
+    auto *t = new HostTransport();
+    t->cb = cb;
+    t->world = world;
+    t->rank = rank;
+    return t;
+}
+
 void make_plan(int n, int G, int r, ShardPlan &P)
 {
     Geom g;

@@ -14,6 +14,7 @@
 
 #include <vector>
 
+#include "../../include/qap_rlt2.h"
 #include "rlt2_internal.h"
 
 namespace rlt2 {
@@ -46,6 +47,8 @@ struct Transport {
     virtual const char *error() const = 0;
 };
 
+// Host-staged: device buffers -> pinned host -> the caller's callbacks -> device.
+Transport *make_host_transport(const qap_host_transport &cb, int world, int rank);
 // NCCL (dlopen'd libnccl.so.2): nullptr if NCCL is unavailable; `err` says why.
 Transport *make_nccl_transport(const void *unique_id, int world, int rank, int device, const char **err);
 // 128-byte ncclUniqueId (rank 0 creates it, the caller broadcasts it to the other ranks).

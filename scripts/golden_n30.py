@@ -9,7 +9,7 @@ D{ij,kl} (i < k; canonical block order, include/qap_rlt2.h export layout) after 
 their sum and max, so that a GPU test can compare the whole 2.4 GB tensor without the oracle.
 Nothing here comes from the CUDA path.
 
-    python scripts/golden_n30.py            # ~4 min of one core
+    python scripts/golden_n30.py            # ~6 min of one core, ~1 min of 8
 """
 import hashlib
 import json
@@ -48,6 +48,7 @@ def group_digests(D, n):
 
 def main():
     oracle.build()
+    oracle.set_threads(os.cpu_count() or 1)   # bit-identical for every thread count
     inst = qapgen.nug(N, SEED)
     st = oracle.State(inst.F, inst.D)
     t0 = time.time()

@@ -100,9 +100,11 @@ def test_flag_constants_match_header(pkg):
 
 
 def test_tensor_tma_in_sass(pkg):
-    """The transfers move boxes with tensor-map TMA; the class-layout LAP gathers rows with
-    tile::gather4 / tile::scatter4 (sm_100a)."""
+    """The transfer loads its boxes with tensor-map TMA (4-D maps); the LAP kernel moves
+    whole cost blocks with 1-D bulk copies both ways and takes its argmins with redux.sync
+    (sm_100a)."""
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", pkg.LIB_PATH],
                           capture_output=True, text=True).stdout
-    assert "UTMALDG.4D" in sass and "UTMASTG.4D" in sass
-    assert "UTMALDG.2D.GATHER4" in sass and "UTMASTG.2D.SCATTER4" in sass
+    assert "UTMALDG.4D" in sass
+    assert "UBLKCP.S.G" in sass and "UBLKCP.G.S" in sass
+    assert "REDUX.MIN.S32" in sass and "MATCH.ANY" in sass

@@ -417,7 +417,18 @@ def test_bnb_checkpoint_resume(orc, torch, pkg, tmp_path, sb):
     with pytest.raises(pkg.QapError):
         pkg.qap_bnb_run(h2, 2, batch=4, sb_iters=sb, checkpoint_path=path, resume=True)
     pkg.qap_destroy(h2)
+    # a checkpoint of a subtree search only resumes that subtree (same root pairs)
+    root = {"fac": [0], "loc": [2], "lb": float("nan")}
+    sub = pkg.qap_bnb_run(h, 2, batch=2, sb_iters=sb, root=root, checkpoint_path=path, max_nodes=3)
+    assert not sub["complete"]
+    for bad in (None, {"fac": [0], "loc": [3], "lb": float("nan")}):
+        with pytest.raises(pkg.QapError):
+            pkg.qap_bnb_run(h, 2, batch=2, sb_iters=sb, root=bad, checkpoint_path=path, resume=True)
+    rs = pkg.qap_bnb_run(h, 2, batch=2, sb_iters=sb, root=root, checkpoint_path=path, resume=True)
+    whole = pkg.qap_bnb_run(h, 2, batch=2, sb_iters=sb, root=root)
+    assert rs["complete"] and all(rs[k] == whole[k] for k in keys)
     pkg.qap_destroy(h)
+    assert not os.path.exists(path + ".tmp")
 
 
 @pytest.mark.gpu
