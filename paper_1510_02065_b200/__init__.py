@@ -63,10 +63,20 @@ class QapError(RuntimeError):
         self.status = status
 
 
+_XchgFn = ct.CFUNCTYPE(ct.c_int32, ct.c_void_p, ct.POINTER(ct.c_double), ct.POINTER(ct.c_double),
+                       ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64), ct.c_int32, ct.c_int32)
+_GatherFn = ct.CFUNCTYPE(ct.c_int32, ct.c_void_p, ct.POINTER(ct.c_double), ct.POINTER(ct.c_int64), ct.c_int32,
+                         ct.c_int32)
+
+
+class _HostTransport(ct.Structure):
+    _fields_ = [("ctx", ct.c_void_p), ("exchange", _XchgFn), ("allgather", _GatherFn)]
+
+
 class _Opts(ct.Structure):
     _fields_ = [("device", ct.c_int32), ("cuda_stream", ct.c_void_p), ("flags", ct.c_int32),
                 ("lap_warps", ct.c_int32), ("world", ct.c_int32), ("rank", ct.c_int32),
-                ("nccl_id", ct.c_void_p)]
+                ("nccl_id", ct.c_void_p), ("host_transport", ct.POINTER(_HostTransport))]
 
 
 class _Result(ct.Structure):
@@ -163,10 +173,46 @@ class Handle:
         self.close()
 
 
+def host_transport(exchange, allgather):
+    """qap_host_transport from two Python callables (argument marshalling only; the library
+    stages its buffers to host memory around each call):
+      exchange(send, recv, off, count, world, rank): numpy float64 views of the staged
+        buffers and int64 arrays of per-peer offsets / counts (doubles);
+      allgather(S_all, lo, world, rank): S_all in place, lo[world + 1].
+    Keep the returned object alive as long as the handle (qap_rlt2_create does)."""
+    def _x(_ctx, send, recv, off, cnt, world, rank):
+        try:
+            o = np.ctypeslib.as_array(off, (world,)).copy()
+            c = np.ctypeslib.as_array(cnt, (world,)).copy()
+            n = int((o + c).max()) if world else 0
+            exchange(np.ctypeslib.as_array(send, (max(n, 1),)), np.ctypeslib.as_array(recv, (max(n, 1),)), o, c,
+                     world, rank)
+            return 0
+        except BaseException:  # noqa: BLE001 - reported as a failed collective
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    def _g(_ctx, S, lo, world, rank):
+        try:
+            lo_ = np.ctypeslib.as_array(lo, (world + 1,)).copy()
+            allgather(np.ctypeslib.as_array(S, (max(int(lo_[-1]), 1),)), lo_, world, rank)
+            return 0
+        except BaseException:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    t = _HostTransport(None, _XchgFn(_x), _GatherFn(_g))
+    t._keep = (t.exchange, t.allgather)
+    return t
+
+
 def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0, lap_warps: int = 0,
-                    world: int = 1, rank: int = 0, nccl_id: bytes | None = None) -> Handle:
+                    world: int = 1, rank: int = 0, nccl_id: bytes | None = None, transport=None) -> Handle:
     """world > 1: this process's shard of one bound shared by `world` processes (collective;
-    nccl_id = qap_nccl_unique_id() from rank 0, broadcast by the caller)."""
+    nccl_id = qap_nccl_unique_id() from rank 0, broadcast by the caller; or transport =
+    host_transport(...) for host-staged collectives)."""
     L = load_library()
     F = np.ascontiguousarray(F, dtype=np.int64)
     D = np.ascontiguousarray(D, dtype=np.int64)
@@ -174,11 +220,14 @@ def qap_rlt2_create(N: int, F, D, device: int = -1, stream=None, flags: int = 0,
         raise ValueError("F and D must be N×N")
     idbuf = ct.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
     opts = _Opts(device, stream if stream is not None else _current_stream(), flags, lap_warps, world, rank,
-                 ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None)
+                 ct.cast(idbuf, ct.c_void_p) if idbuf is not None else None,
+                 ct.pointer(transport) if transport is not None else None)
     out = ct.c_void_p()
     st = L.qap_rlt2_create(N, F.ctypes.data, D.ctypes.data, ct.byref(opts), ct.byref(out))
     _check(st, None)
-    return Handle(out.value, N, world)
+    h = Handle(out.value, N, world)
+    h._transport = transport  # the callbacks must outlive the handle
+    return h
 
 
 def qap_rlt2_load(h: Handle, F, D) -> None:

@@ -132,3 +132,65 @@ def test_gloo_world2_exchange_layout(pkg, n):
         pr.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
     assert res[0][2] == res[1][2] > 0
+
+
+def _hostcomm_worker(rank, world, port, n, q):
+    """The host-staged transport's callbacks (paper_1510_02065_b200/hostcomm.py) over gloo,
+    driven exactly as the library drives them: staged slot buffers with the plan's per-peer
+    offsets / counts, then the rank-major all-gather of level-2 values."""
+    import ctypes as ct
+
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1510_02065_b200 as pkg
+        from paper_1510_02065_b200.hostcomm import process_group_transport
+        t = process_group_transport()
+        p = pkg.qap_shard_plan(n, world, rank)
+        kSlot = 512
+        slots = p["peer_slots"].astype(np.int64)
+        off = np.concatenate([[0], np.cumsum(slots)[:-1]]).astype(np.int64) * kSlot
+        cnt = slots * kSlot
+        cnt[rank] = 0
+        send = np.full(int(slots.sum()) * kSlot + 1, -1.0)
+        for tid, kind, slot in zip(p["tiles"], p["kind"], p["slot"]):
+            if kind:
+                send[slot * kSlot:(slot + 1) * kSlot] = float(tid)
+        recv = np.zeros_like(send)
+        dp = ct.POINTER(ct.c_double)
+        ip = ct.POINTER(ct.c_int64)
+        rc = t.exchange(None, send.ctypes.data_as(dp), recv.ctypes.data_as(dp), off.ctypes.data_as(ip),
+                        cnt.ctypes.data_as(ip), world, rank)
+        ok = rc == 0
+        for tid, kind, slot in zip(p["tiles"], p["kind"], p["slot"]):
+            if kind:
+                ok &= bool((recv[slot * kSlot:(slot + 1) * kSlot] == float(tid)).all())
+        lo = p["blk_lo"].astype(np.int64)
+        S = np.full(int(lo[-1]), -1.0)
+        S[lo[rank]:lo[rank + 1]] = np.arange(lo[rank], lo[rank + 1], dtype=np.float64)
+        rc = t.allgather(None, S.ctypes.data_as(dp), lo.ctypes.data_as(ip), world, rank)
+        ok &= rc == 0 and bool((S == np.arange(lo[-1], dtype=np.float64)).all())
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [7, 12])
+def test_gloo_world2_host_transport(pkg, n):
+    """world_size 2 on CPU: the host transport's exchange delivers every shared tile's slots
+    to its partner and the all-gather leaves every rank with all level-2 values."""
+    import torch.multiprocessing as mp
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_hostcomm_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(ok for _, ok in res), res
