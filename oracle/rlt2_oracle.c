@@ -102,18 +102,27 @@ int oracle_lap(int m, const double *M, double *R, int32_t *assign, double *u_out
         if (p[a] == 0) { p[a] = r; rmatched[r] = 1; }
     }
 
-    /* the remaining rows, ascending, each by one shortest-augmenting-path search */
+    /* the remaining rows, ascending, each by one shortest-augmenting-path search: Dijkstra
+     * over the reduced costs from row i, with tentative distances minv[j] and the distance
+     * dist[j] of every column when it is settled; the potentials change once, at the end of
+     * the search (the augmentation of Jonker & Volgenant): every settled column j moves by
+     * dfin - dist[j], dfin = the distance of the free column reached.  In exact arithmetic
+     * this is the textbook step-by-step update (u[p[j]] += delta, v[j] -= delta for the used
+     * columns after every step).                                                          */
+    double *dist = malloc(((size_t)m + 1) * sizeof(double));
     for (int i = 1; i <= m; i++) {
         if (rmatched[i]) continue;
         p[0] = i;
         int j0 = 0;
         for (int j = 0; j <= m; j++) { minv[j] = INFINITY; used[j] = 0; }
+        dist[0] = 0.0;
         do {
             used[j0] = 1;
             int i0 = p[j0];
+            const double c = dist[j0] - u[i0];      /* distance of row i0 minus its potential */
             for (int j = 1; j <= m; j++) {
                 if (used[j]) continue;
-                double cur = (M[(size_t)(i0 - 1) * m + (j - 1)] - u[i0]) - v[j];
+                double cur = (M[(size_t)(i0 - 1) * m + (j - 1)] - v[j]) + c;
                 if (cur < minv[j]) { minv[j] = cur; way[j] = j0; }
             }
             int j1 = -1;
@@ -123,16 +132,20 @@ int oracle_lap(int m, const double *M, double *R, int32_t *assign, double *u_out
                     (minv[j] == minv[j1] && p[j] == 0 && p[j1] != 0))
                     j1 = j;
             }
-            double delta = minv[j1];
-            for (int j = 0; j <= m; j++) {
-                if (used[j]) { u[p[j]] += delta; v[j] -= delta; }
-                else         { minv[j] -= delta; }
-            }
+            dist[j1] = minv[j1];
             j0 = j1;
             steps++;
         } while (p[j0] != 0);
+        const double dfin = dist[j0];
+        for (int j = 0; j <= m; j++) {
+            if (!used[j]) continue;
+            const double t = dfin - dist[j];
+            u[p[j]] = u[p[j]] + t;
+            v[j] = v[j] - t;
+        }
         do { int j1 = way[j0]; p[j0] = p[j1]; j0 = j1; } while (j0);
     }
+    free(dist);
 
     int32_t *a = malloc((size_t)m * sizeof(int32_t));
     for (int j = 1; j <= m; j++) a[p[j] - 1] = j - 1;

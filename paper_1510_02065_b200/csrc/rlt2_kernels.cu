@@ -293,7 +293,6 @@ __device__ __forceinline__ void warp_lap_solve(const double *M, int m, int lane,
 {
     const double *Mlane = M + lane;
     double minv[CPL];
-    double du[CPL];  // 1.0 on settled columns, else 0.0: fma(delta, du, x) == x + delta exactly
     int way[CPL];
     const int rowb = m * 8;
     int col[CPL];
@@ -308,21 +307,24 @@ __device__ __forceinline__ void warp_lap_solve(const double *M, int m, int lane,
     munkres_init<CPL>(M, m, lane, col, scratch, poff, ucol, rmin, rmask);
     for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
         if ((sel_t<CPL>(rmask, i >> 5) >> (i & 31)) & 1u) continue;  // matched by the row reduction
-        // u of row i = u[p[dummy]]: its row minimum
-        double ucur = __shfl_sync(FULL_MASK, sel_t<CPL>(rmin, i >> 5), i & 31);
+        // u of row i = u[p[dummy]]: its row minimum.  Dijkstra from row i with absolute
+        // tentative distances (minv); the scanned row i0 enters as c = dist(its column) -
+        // u[i0]; the potentials move once, after the search (as warp_lap_solve1).
+        const double ui = __shfl_sync(FULL_MASK, sel_t<CPL>(rmin, i >> 5), i & 31);
+        uint32_t dhi[CPL];  // settled: high word of the column's distance (low word stays in minv)
 #pragma unroll
         for (int t = 0; t < CPL; t++) {
             minv[t] = (lane + 32 * t) < m ? CUDART_INF : qnan();
-            du[t] = 0.0;
+            dhi[t] = 0xffffffffu;
         }
         int j0 = -1, i0off = i * rowb;
-        double ui0 = ucur;
+        double c = 0.0 - ui, dfin;
         int jfree;
         while (true) {
             const double *row = reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off);
 #pragma unroll
             for (int t = 0; t < CPL; t++) {
-                const double cur = (row[32 * t] - ui0) - v[t];
+                const double cur = (row[32 * t] - v[t]) + c;
                 if (cur < minv[t]) {  // false for settled columns (minv = NaN)
                     minv[t] = cur;
                     way[t] = j0;
@@ -330,33 +332,40 @@ __device__ __forceinline__ void warp_lap_solve(const double *M, int m, int lane,
             }
             int j1;
             bool j1free;
-            double delta;
+            double delta;  // minv of column j1: its distance
             warp_argmin<CPL>(minv, poff, j1, j1free, delta);
-            // next row to scan (used only if j1 is matched): fetched with the same lane group
-            // as delta; ucol[j1] is not touched by this step's update (j1 is not yet settled)
+            // next row to scan (used only if j1 is matched): its offset and u
             const int src = j1 & 31, tt = j1 >> 5;
             const int nx_off = __shfl_sync(FULL_MASK, sel_t<CPL>(poff, tt), src);
             const double nx_u = __shfl_sync(FULL_MASK, sel_t<CPL>(ucol, tt), src);
-            ucur += delta;
 #pragma unroll
             for (int t = 0; t < CPL; t++) {
-                minv[t] -= delta;                   // NaN stays NaN on settled columns
-                ucol[t] = fma(delta, du[t], ucol[t]);  // settled: u[p[j]] += delta (exact product)
-                v[t] = fma(-delta, du[t], v[t]);       // settled: v[j] -= delta
-                if (lane + 32 * t == j1) {  // settle column j1: only the high words change
-                    du[t] = __hiloint2double(0x3ff00000, __double2loint(du[t]));
+                if (lane + 32 * t == j1) {  // settle column j1
+                    dhi[t] = static_cast<uint32_t>(__double2hiint(minv[t]));
                     minv[t] = __hiloint2double(0x7ff80000, __double2loint(minv[t]));
                 }
             }
             if (COUNT) steps++;
             if (j1free) {
                 jfree = j1;
+                dfin = delta;
                 break;
             }
             i0off = nx_off;
-            ui0 = nx_u;
+            c = delta - nx_u;
             j0 = j1;
         }
+        // potentials: every column settled in this search moves by dfin - dist (the free end
+        // column by +0); row i's u by dfin
+#pragma unroll
+        for (int t = 0; t < CPL; t++) {
+            if (dhi[t] != 0xffffffffu) {
+                const double tt = dfin - __hiloint2double(static_cast<int>(dhi[t]), __double2loint(minv[t]));
+                ucol[t] = ucol[t] + tt;
+                v[t] = v[t] - tt;
+            }
+        }
+        const double ucur = ui + dfin;
         // augment along way[]: columns on the path take the row (and its u) of way[c].
         // The path (a few columns) is walked once with warp-uniform values; its columns are
         // collected in a bit mask per column group t.
@@ -452,11 +461,14 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
     for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
         if ((rmask[0] >> i) & 1u) continue;  // matched by the row reduction
         const double ui = __shfl_sync(FULL_MASK, rmin, i);  // u of row i: its row minimum
-        double ucur = ui, ui0 = ui, minv = minv0, du = 0.0;
+        // Dijkstra from row i with absolute tentative distances (minv); the scanned row i0
+        // enters as c = dist(its column) - u[i0]; potentials move once, after the search
+        double minv = minv0, c = 0.0 - ui;
+        uint32_t dhi = 0xffffffffu;  // settled: high word of the column's distance (low word stays in minv)
         int j0 = -1, i0off = i * rowb, j1;
 #pragma unroll 2
         for (;;) {
-            const double cur = (*reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off) - ui0) - v;
+            const double cur = (*reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off) - v) + c;
             if (cur < minv) {  // false for settled columns (minv = NaN)
                 minv = cur;
                 way = j0;
@@ -476,23 +488,28 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
                 j1 = hibit(fb ? fb : bal);  // a free column first; highest lane = lowest column
             }
             const uint32_t ft = bal & freemask;
-            const double delta = __shfl_sync(FULL_MASK, minv, j1);
+            const double cj = minv - ucol;  // lane j1: dist[j1] - u[p[j1]], the next row's offset
+            const double nc = __shfl_sync(FULL_MASK, cj, j1);
             const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
-            const double nx_u = __shfl_sync(FULL_MASK, ucol, j1);
-            ucur += delta;
-            minv -= delta;                  // NaN stays NaN on settled columns
-            ucol = fma(delta, du, ucol);    // settled: u[p[j]] += delta (exact product)
-            v = fma(-delta, du, v);         // settled: v[j] -= delta
-            if (lane == j1) {               // settle column j1: only the high words change
-                du = __hiloint2double(0x3ff00000, __double2loint(du));
+            if (lane == j1) {  // settle column j1: keep its distance's high word, NaN in minv
+                dhi = static_cast<uint32_t>(__double2hiint(minv));
                 minv = __hiloint2double(0x7ff80000, __double2loint(minv));
             }
             if (COUNT) steps++;
             if (ft) break;
             i0off = nx_off;
-            ui0 = nx_u;
+            c = nc;
             j0 = j1;
         }
+        // potentials: every column settled in this search moves by dfin - dist (the free end
+        // column by +0); row i's u by dfin
+        const double dfin = __shfl_sync(FULL_MASK, __hiloint2double(static_cast<int>(dhi), __double2loint(minv)), j1);
+        if (dhi != 0xffffffffu) {
+            const double t = dfin - __hiloint2double(static_cast<int>(dhi), __double2loint(minv));
+            ucol = ucol + t;
+            v = v - t;
+        }
+        const double ucur = ui + dfin;
         // augment along way[]: columns on the path take the row (and its u) of way[c]
         freemask &= ~(1u << j1);
         uint32_t onmask = 0u;
