@@ -305,8 +305,13 @@ __device__ __forceinline__ void warp_lap_solve(const double *M, int m, int lane,
     double rmin[CPL];
     uint32_t rmask[CPL];
     munkres_init<CPL>(M, m, lane, col, scratch, poff, ucol, rmin, rmask);
-    for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
-        if ((sel_t<CPL>(rmask, i >> 5) >> (i & 31)) & 1u) continue;  // matched by the row reduction
+    // the rows the row reduction left unmatched, ascending (P:205 Hungarian, one augmentation
+    // per row)
+    uint64_t um = ~static_cast<uint64_t>(rmask[0]);
+    if (CPL > 1) um &= ~(static_cast<uint64_t>(rmask[CPL - 1]) << 32);
+    if (m < 64) um &= (1ull << m) - 1ull;
+    for (; um; um &= um - 1ull) {
+        const int i = __ffsll(static_cast<long long>(um)) - 1;
         // u of row i = u[p[dummy]]: its row minimum.  Dijkstra from row i with absolute
         // tentative distances (minv); the scanned row i0 enters as c = dist(its column) -
         // u[i0]; the potentials move once, after the search (as warp_lap_solve1).
@@ -458,8 +463,10 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
     const double rmin = rm[0];
     // lanes 32-m .. 31 hold columns; those matched by the row reduction are taken
     uint32_t freemask = (m >= 32 ? 0xffffffffu : ~((1u << (32 - m)) - 1u)) & ~__ballot_sync(FULL_MASK, poff >= 0);
-    for (int i = 0; i < m; i++) {  // insert row i (P:205 Hungarian, one augmentation per row)
-        if ((rmask[0] >> i) & 1u) continue;  // matched by the row reduction
+    // the rows the row reduction left unmatched, ascending (P:205 Hungarian, one augmentation
+    // per row)
+    for (uint32_t um = ~rmask[0] & (m >= 32 ? 0xffffffffu : ((1u << m) - 1u)); um; um &= um - 1u) {
+        const int i = __ffs(um) - 1;
         const double ui = __shfl_sync(FULL_MASK, rmin, i);  // u of row i: its row minimum
         // Dijkstra from row i with absolute tentative distances (minv); the scanned row i0
         // enters as c = dist(its column) - u[i0]; potentials move once, after the search
