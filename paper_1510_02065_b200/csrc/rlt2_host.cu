@@ -6,6 +6,7 @@
 // the remaining launches of the call into no-ops, so a bound call synchronises once.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <fcntl.h>
 #include <unistd.h>
@@ -92,6 +93,13 @@ struct qap_rlt2 {
     // tensor maps of D for k_transfer_tma, encoded for node size tma_n (0: none / failed)
     TmaMaps tma{};
     int tma_n = 0;
+};
+
+// NVTX range around the host-side enqueue of a phase / call (SURVEY §5 tracing): visible in
+// any NVTX-aware profiler, a no-op without one (header-only nvtx3, no link dependency)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 static std::string g_create_error;
@@ -380,6 +388,7 @@ qap_status qap_rlt2_load(qap_rlt2 *h, const int64_t *F, const int64_t *D)
 
 qap_status qap_rlt2_fix(qap_rlt2 *h, int32_t m, const int32_t *fac, const int32_t *loc)
 {
+    NvtxRange nv("qap_rlt2_fix");
     if (!h) return QAP_E_ARG;
     const int N = h->N;
     if (m < 0 || N - m < 3) return fail(h, QAP_E_ARG, "need 0 <= m <= N-3");
@@ -601,8 +610,13 @@ static bool tma_maps(qap_rlt2 *h)
 }
 
 // Enqueue one phase of Algorithm 1.  `st` is the stream the call's work is ordered on.
+static const char *const kPhaseName[] = {"rlt2 iteration 0 (C->B->LB)", "rlt2 spread + transfer D",
+                                         "rlt2 level-2 LAPs (D->C)", "rlt2 level-1 LAPs (C->B)",
+                                         "rlt2 level-0 LAP (B->LB)"};
+
 static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused)
 {
+    NvtxRange nv(phase >= 0 && phase <= QAP_PHASE_CONC_B ? kPhaseName[phase] : "rlt2 phase");
     cudaError_t e = cudaSuccess;
     const Geom &g = h->geom;
     if (h->world > 1 && (phase == QAP_PHASE_TRANSFER || phase == QAP_PHASE_CONC_D)) {
@@ -708,6 +722,7 @@ qap_status qap_rlt2_bound(qap_rlt2 *h, int32_t max_iters, double K, double UB, q
 
 qap_status qap_rlt2_bound_async(qap_rlt2 *h, int32_t max_iters, double K, double UB)
 {
+    NvtxRange nv("qap_rlt2_bound");
     if (!h) return QAP_E_ARG;
     if (max_iters < 0 || !(K >= 0.0) || std::isnan(UB)) return fail(h, QAP_E_ARG, "bad max_iters/K/UB");
     if (h->next_phase != PH_FRESH && h->next_phase != QAP_PHASE_TRANSFER)
@@ -1635,6 +1650,7 @@ extern "C" {
 
 qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *o, qap_bnb_result *out)
 {
+    NvtxRange nv("qap_bnb_run");
     if (!h || !o || !out || o->iters < 0) return QAP_E_ARG;
     if ((o->resume || o->checkpoint_every > 0) && !o->checkpoint_path)
         return fail(h, QAP_E_ARG, "checkpointing needs checkpoint_path");
