@@ -362,6 +362,9 @@ typedef struct {
     int32_t perm[64];
     int64_t bounded, leaves, pruned, sb_cut;
     int32_t complete;
+    int32_t depth_max;        /* fixed pairs of the deepest expanded node on the DFS stack now */
+    int64_t open;             /* unvisited children on the DFS stack (0 when complete)  */
+    int64_t bounded_by_depth[64];  /* bounded nodes by their number of fixed pairs      */
 } qap_bnb_result;
 qap_status qap_bnb_run(qap_rlt2 *h, const qap_bnb_opts *opts, qap_bnb_result *out);
 

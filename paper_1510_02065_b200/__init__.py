@@ -54,7 +54,8 @@ class _BnbOpts(ct.Structure):
 
 class _BnbResult(ct.Structure):
     _fields_ = [("opt", ct.c_int64), ("perm", ct.c_int32 * 64), ("bounded", ct.c_int64), ("leaves", ct.c_int64),
-                ("pruned", ct.c_int64), ("sb_cut", ct.c_int64), ("complete", ct.c_int32)]
+                ("pruned", ct.c_int64), ("sb_cut", ct.c_int64), ("complete", ct.c_int32),
+                ("depth_max", ct.c_int32), ("open", ct.c_int64), ("bounded_by_depth", ct.c_int64 * 64)]
 
 
 class QapError(RuntimeError):
@@ -359,7 +360,8 @@ def _node_out(x) -> dict:
 
 def _result_out(h: Handle, r) -> dict:
     return dict(opt=r.opt, perm=np.array(r.perm[: h.N], np.int32), bounded=r.bounded, leaves=r.leaves,
-                pruned=r.pruned, sb_cut=r.sb_cut, complete=bool(r.complete))
+                pruned=r.pruned, sb_cut=r.sb_cut, complete=bool(r.complete), open=r.open, depth_max=r.depth_max,
+                bounded_by_depth=[int(x) for x in r.bounded_by_depth[: h.N]])
 
 
 def qap_bnb_run(h: Handle, iters: int, K: float = 0.0, UB0: float = math.inf, batch: int = 1,

@@ -1022,6 +1022,12 @@ struct Bnb {
     int64_t best = -1;
     std::vector<int32_t> best_perm;
     int64_t bounded = 0, leaves = 0, pruned = 0, sb_cut = 0;
+    std::vector<int64_t> bdepth = std::vector<int64_t>(65, 0);  // bounded nodes by fixed pairs
+    void counted(size_t d)
+    {
+        bounded++;
+        if (d < bdepth.size()) bdepth[d]++;
+    }
     std::vector<Frame> stack;
     bool root_done = false;
     qap_status st = QAP_OK;
@@ -1165,7 +1171,7 @@ struct Bnb {
         if ((st = qap_rlt2_fix(depth[0], 0, nullptr, nullptr)) != QAP_OK) return;
         qap_rlt2_result r{};
         if ((st = qap_rlt2_bound(depth[0], iters, K, UB, &r)) != QAP_OK) return;
-        bounded++;
+        counted(0);
         if (r.lb > UB - 1.0 + 1e-6) {
             pruned++;
             return;
@@ -1192,7 +1198,7 @@ struct Bnb {
             if ((st = qap_rlt2_fix(depth[0], root->m, fac.data(), loc.data())) != QAP_OK) return;
             qap_rlt2_result r{};
             if ((st = qap_rlt2_bound(depth[0], iters, K, UB, &r)) != QAP_OK) return;
-            bounded++;
+            counted(root->m);
             lb = r.lb;
         }
         if (cut(lb)) {
@@ -1218,7 +1224,7 @@ struct Bnb {
                     sb_cut++;
                     continue;
                 }
-                bounded++;
+                counted(F.fac.size() + 1);
                 if (cut(F.lb[c])) {
                     pruned++;
                     continue;
@@ -1271,7 +1277,7 @@ struct Bnb {
             leaf(fac, loc);
             return true;
         }
-        bounded++;
+        counted(fac.size());
         if (T.lb[c] > UB - 1.0 + 1e-6) {
             pruned++;
             return true;
@@ -1463,6 +1469,7 @@ bool save_checkpoint(const Bnb &B, const char *path, std::string &err)
     put(o, B.leaves);
     put(o, B.pruned);
     put(o, B.sb_cut);
+    putv(o, B.bdepth);
     put(o, (uint64_t)B.stack.size());
     for (const Frame &F : B.stack) {
         putv(o, F.fac);
@@ -1540,6 +1547,8 @@ bool load_checkpoint(Bnb &B, const char *path, std::string &err)
     B.leaves = R.get<int64_t>();
     B.pruned = R.get<int64_t>();
     B.sb_cut = R.get<int64_t>();
+    B.bdepth = R.getv<int64_t>();
+    if (B.bdepth.size() != 65) R.ok = false;
     const uint64_t nf = R.get<uint64_t>();
     B.stack.clear();
     for (uint64_t k = 0; k < nf && R.ok; k++) {
@@ -1643,6 +1652,11 @@ void bnb_out(const Bnb &b, bool done, qap_bnb_result *out)
     out->leaves = b.leaves;
     out->pruned = b.pruned;
     out->sb_cut = b.sb_cut;
+    int64_t open = 0;
+    for (const Frame &F : b.stack) open += (int64_t)F.fs.size() - (int64_t)F.next;
+    out->open = open;
+    out->depth_max = (int32_t)(b.base_m + b.stack.size());
+    for (int d = 0; d < 64; d++) out->bounded_by_depth[d] = b.bdepth[d];
 }
 }  // namespace
 
@@ -1723,7 +1737,7 @@ qap_status qap_bnb_frontier(qap_rlt2 *h, const qap_bnb_opts *o, int32_t target, 
             if ((b.st = qap_rlt2_fix(h, root.m, fac.data(), loc.data())) != QAP_OK) return b.st;
             qap_rlt2_result r{};
             if ((b.st = qap_rlt2_bound(h, b.iters, b.K, b.UB, &r)) != QAP_OK) return b.st;
-            b.bounded++;
+            b.counted(root.m);
             root.lb = r.lb;
         }
         if (b.cut(root.lb)) b.pruned++;
@@ -1753,7 +1767,7 @@ qap_status qap_bnb_frontier(qap_rlt2 *h, const qap_bnb_opts *o, int32_t target, 
                     b.leaf(fac, loc);
                     continue;
                 }
-                b.bounded++;
+                b.counted(ch.m);
                 if (b.cut(F.lb[c])) {
                     b.pruned++;
                     continue;
