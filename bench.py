@@ -387,6 +387,26 @@ def main():
                                  "note": "children folded from the parent's dual state (NEXT-3)"}}
     pkg.qap_destroy(h)
 
+    # B&B at N = 20 (BASELINE config 3's size; tai*b-shaped like the paper's tai20b): a full
+    # solve to proven optimality with strong branching, on rank 0
+    bnb20 = None
+    if not args.no_bnb and rank == 0:
+        bi = qapgen.taib(20, SEED)
+        hb = pkg.qap_rlt2_create(20, bi.F, bi.D, device=local_rank, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r20 = pkg.qap_bnb_run(hb, BNB_ITERS, batch=20, sb_iters=1)
+        torch.cuda.synchronize()
+        dt20 = time.perf_counter() - t0
+        pkg.qap_destroy(hb)
+        assert r20["complete"] and bi.evaluate([int(x) for x in r20["perm"]]) == r20["opt"]
+        bnb20 = {"config": f"tai20b-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node, strong "
+                           "branching (RLT1, 1 iteration), children bounded 20 at a time, UB0=inf",
+                 "opt": r20["opt"], "bounded_nodes": r20["bounded"], "leaves": r20["leaves"],
+                 "pruned": r20["pruned"], "cut_by_rlt1": r20["sb_cut"], "seconds": dt20,
+                 "nodes_per_s": r20["bounded"] / dt20, "bounded_by_depth": r20["bounded_by_depth"],
+                 "timer": "host wall clock of one cold solve (first call: helper handles and graphs included)"}
+
     # subtree-parallel B&B: one worker per GPU on a larger tree;
     # at N=1 the same instance by the batched DFS of one GPU (the scaling reference)
     sub = None
@@ -503,7 +523,7 @@ def main():
                     "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 80,
                     "path": "per step: qap_rlt2_load(pinned host F, D) + qap_rlt2_bound(T=20) "
                             "(result read back to the host)"},
-            "bnb": bnb, "bnb_subtree": sub,
+            "bnb": bnb, "bnb_n20": bnb20, "bnb_subtree": sub,
             "gpu_launches": launches,
             "clocks": clk.summary()}
     if world == 1 and not args.no_cpu_baseline:
