@@ -1619,8 +1619,10 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
     b.depth.push_back(h);
     const int B = o->batch < 1 ? 1 : (o->batch > b.N ? b.N : o->batch);
     int nh = b.warm ? B : B - 1;  // warm: the caller's handle keeps the root's state
-    // helpers bound children only (at most N - 1 free facilities); when device memory runs out
-    // (large N: one handle holds the N^6/2 tensor), fewer children are bounded at a time
+    // helpers bound children (at most N - 1 free facilities), except that the first one also
+    // hosts the strong-branching RLT1 batch of an expanded node in warm mode (pool[0]), which
+    // needs the node's own size; when device memory runs out (large N: one handle holds the
+    // N^6/2 tensor), fewer children are bounded at a time
     while ((int)h->bnb_helpers.size() < nh) {
         cudaStream_t s = nullptr;
         cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
@@ -1631,7 +1633,8 @@ qap_status bnb_init(qap_rlt2 *h, const qap_bnb_opts *o, Bnb &b)
         op.flags = h->flags & ~QAP_FLAG_TIME_KERNELS;
         op.lap_warps = h->lap_warps;
         qap_rlt2 *x = nullptr;
-        qap_status st = create_impl(h->N, h->F.data(), h->Dist.data(), &op, &x, false, h->N - 1);
+        const int cap = h->bnb_helpers.empty() ? h->N : h->N - 1;
+        qap_status st = create_impl(h->N, h->F.data(), h->Dist.data(), &op, &x, false, cap);
         if (st != QAP_OK) {
             cudaStreamDestroy(s);
             if (st == QAP_E_CAPACITY && (b.warm ? (int)h->bnb_helpers.size() >= 1 : true)) {

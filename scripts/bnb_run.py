@@ -78,6 +78,7 @@ def main():
     ap.add_argument("--warm", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="children bounded concurrently (0: N)")
     ap.add_argument("--ub0", type=float, default=float("inf"))
+    ap.add_argument("--K", type=float, default=0.0, help="stop a node's ascent when LB'/UB < K (R14)")
     ap.add_argument("--chunk", type=int, default=200)
     ap.add_argument("--budget-s", type=float, default=600)
     ap.add_argument("--ckpt", default=None)
@@ -95,7 +96,7 @@ def main():
         os.remove(ckpt)
     out = open(a.out, "a") if a.out else None
     cfg = {"instance": f"{a.family}{a.n}-shaped seed {a.seed}", "N": a.n, "iters_per_node": a.iters,
-           "strong_branching": a.sb, "warm_children": a.warm, "batch": a.batch or a.n, "UB0": a.ub0}
+           "strong_branching": a.sb, "warm_children": a.warm, "batch": a.batch or a.n, "UB0": a.ub0, "K": a.K}
 
     def emit(d):
         line = json.dumps(d)
@@ -108,7 +109,7 @@ def main():
     t0 = time.perf_counter()
     first, r, last_b, last_t = True, None, 0, t0
     while True:
-        r = pkg.qap_bnb_run(h, a.iters, UB0=a.ub0, batch=a.batch or a.n, sb_iters=a.sb, warm=a.warm,
+        r = pkg.qap_bnb_run(h, a.iters, K=a.K, UB0=a.ub0, batch=a.batch or a.n, sb_iters=a.sb, warm=a.warm,
                             checkpoint_path=ckpt, max_nodes=a.chunk, resume=not first)
         first = False
         torch.cuda.synchronize()
