@@ -480,6 +480,7 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
                 minv = cur;
                 way = j0;
             }
+            const double cj = minv - ucol;  // lane j1 (below): dist[j1] - u[p[j1]], the next row's offset
             // argmin of (minv, matched?, column).  While no minv is negative (Dijkstra
             // distances are >= 0 up to rounding; settled columns hold +NaN) the raw high words
             // order the values as signed integers (and equal high words by their low words as
@@ -495,7 +496,6 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
                 j1 = hibit(fb ? fb : bal);  // a free column first; highest lane = lowest column
             }
             const uint32_t ft = bal & freemask;
-            const double cj = minv - ucol;  // lane j1: dist[j1] - u[p[j1]], the next row's offset
             const double nc = __shfl_sync(FULL_MASK, cj, j1);
             const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
             if (lane == j1) {  // settle column j1: keep its distance's high word, NaN in minv
@@ -543,20 +543,24 @@ template <int CPL, class GVal>
 __device__ __forceinline__ double warp_lap_epilogue(double *M, GVal Mg, int m, int ldm, const int (&cofs)[CPL],
                                                     int lane, int col0, const int (&poff)[CPL], int (&p)[CPL],
                                                     const double (&v)[CPL], const double (&ucol)[CPL], double *urow,
-                                                    double *sel, int ust, bool &bad)
+                                                    double *sel, int ust, uint32_t rmag, bool &bad)
 {
-    const int rowb = ldm * 8;
+    // poff is a multiple of the row's bytes (8 ldm): the row by a multiply-high with rmag =
+    // ceil(2^32 / (8 ldm)) (exact: poff < 2^32 / (8 ldm))
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         const int c = col0 + 32 * t;
-        p[t] = c < m ? poff[t] / rowb : -1;
+        p[t] = c < m ? (int)__umulhi((uint32_t)poff[t], rmag) : -1;
         if (c < m) {
             urow[p[t] * ust] = ucol[t];
             sel[p[t] * ust] = M[p[t] * ldm + cofs[t]];
         }
     }
     __syncwarp();
-    bool neg = false;  // some raw residual below -1e-9 (<= -tau candidates)
+    // the largest raw high word as unsigned: a value at or above the high word of -1e-9 marks
+    // a residual that may fall below -tau (every negative double with |x| >= 1e-9 has it; the
+    // rare exact test below decides)
+    uint32_t hmax = 0u;
 #pragma unroll
     for (int t = 0; t < CPL; t++) {
         const int c = col0 + 32 * t;
@@ -566,10 +570,10 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, GVal Mg, int m, i
 #pragma unroll 4
             for (int r = 0; r < m; r++) {
                 const double x = (Mc[r * ldm] - urow[r * ust]) - vc;
-                neg |= x < -1e-9;
                 // x <= 0 (incl. -0) -> +0, else x (== x > 0.0 ? x : 0.0 for every non-NaN x):
                 // clear both words when the sign bit is set
                 const int hi = __double2hiint(x), lo = __double2loint(x), keep = ~(hi >> 31);
+                hmax = max(hmax, static_cast<uint32_t>(hi));
                 Mc[r * ldm] = __hiloint2double(hi & keep, lo & keep);
             }
             Mc[p[t] * ldm] = 0.0;  // assigned cell -> +0
@@ -580,7 +584,7 @@ __device__ __forceinline__ double warp_lap_epilogue(double *M, GVal Mg, int m, i
         for (int r = 0; r < m; r++) S = S + sel[r * ust];  // sequential row order (reading R9)
     S = __shfl_sync(FULL_MASK, S, 0);
     bad = false;
-    if (__any_sync(FULL_MASK, neg)) {  // rare: exact test tau = 1e-9 max(1, max|M|)
+    if (__any_sync(FULL_MASK, hmax >= 0xBE112E0Bu)) {  // rare (hi(-1e-9)): exact test tau = 1e-9 max(1, max|M|)
         // recompute the raw residuals from the original block (same operations)
         double mx = 0.0, mn = 0.0;
 #pragma unroll
@@ -699,6 +703,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
     }
     if (b >= a.count) return;
     const uint32_t bytes = (uint32_t)(((int64_t)m * m + 1) & ~int64_t(1)) * 8u;
+    const uint32_t rmag = (uint32_t)((0x100000000ull + (uint64_t)(m * 8) - 1ull) / (uint64_t)(m * 8));
     int icur = 0;  // canonical first facility of block b (L2), advanced monotonically
     int cofs[CPL];      // offset of each owned column within a cost-buffer row
 #pragma unroll
@@ -742,7 +747,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
         const double *Mg = a.src + b * a.ld;
         const double S = warp_lap_epilogue<CPL>(
             M, [&](int r, int t, int c) { return c < m ? Mg[r * m + c] : 0.0; }, m, m, cofs, lane, col0, poff, p, v,
-            ucol, urow, sel, 1, bad);
+            ucol, urow, sel, 1, rmag, bad);
         anybad |= bad;
         if (lane == 0) {
             tma_store_1d(a.dst + b * a.ld, M, bytes);  // residual block back to global
