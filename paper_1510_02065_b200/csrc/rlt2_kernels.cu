@@ -1,16 +1,20 @@
 // rlt2_kernels.cu — sm_100a kernels of the RLT2 dual-ascent bound.
 //
-// P:n = /root/reference/PAPER.md line n.  Readings R1..R30 are listed in DESIGN.md §3.
+// P:n = /root/reference/PAPER.md line n.  Readings R1..R31 are listed in DESIGN.md §3.
 //
-//   k_init      O0/O1: reduced costs of the node                HBM write of B, C
-//   k_sigma     spreading B->C and the per-block C->D spread amount
-//   k_transfer  spreading C->D fused with the transfer between complementary
-//               costs of D: one CTA per facility triple
-//               and 8×8×8 location tile, every class read/written once         HBM-bound
-//   k_lap<CPL>  cost concentration: one warp per LAP, cost
-//               block staged global->smem by a TMA bulk copy, double buffered;
-//               shortest-augmenting-path Hungarian with lane = column, argmin
-//               by two redux.sync.min.u32 on an order-preserving fp64 key     issue/HBM-bound
+//   k_init          O0/O1: reduced costs of the node            HBM write of B, C
+//   k_sigma         spreading B->C and the per-block C->D spread amount
+//   k_transfer_tma  spreading C->D fused with the transfer between complementary
+//                   costs of D: one CTA per facility triple and
+//                   8x8x8 location tile, the three member views as tensor-map TMA boxes
+//   k_transfer      the same with register loads (small nodes, sharded handles)
+//   k_lap<CPL>      cost concentration: one warp per LAP, the cost
+//                   block staged global->smem by a TMA bulk copy and stored back by one;
+//                   Munkres row reduction, then shortest augmenting paths (Jonker-Volgenant
+//                   form) with lane = column, argmin by a signed redux.sync on the raw
+//                   fp64 high word (the low word and the order-preserving key only on ties
+//                   or negative values)                                        issue-bound
+//   k_fold_*, k_rlt1_*, k_credit: warm children, strong branching, sharded credit
 //
 // Arithmetic order follows DESIGN.md §3 exactly (same IEEE operations as the paper's
 // algorithm written out), so results are reproducible bit for bit; no multiplies
