@@ -450,3 +450,21 @@ def test_bnb_config2_n12(torch, pkg, variant):
     assert (r["bounded"], r["leaves"], r["pruned"]) == (o["bounded"], o["leaves"], o["pruned"])
     if variant == "strong_branching":
         assert r["sb_cut"] == o["sb_cut"]
+
+
+def test_bnb_depth_counters_and_open(torch, pkg, tmp_path):
+    """The B&B result's bounded-by-depth histogram sums to the bounded count (and survives a
+    checkpoint/resume); a complete search leaves no open node; an interrupted one reports the
+    unvisited children on its DFS stack."""
+    inst = qapgen.taib(10, 2)
+    h = pkg.qap_rlt2_create(10, inst.F, inst.D)
+    full = pkg.qap_bnb_run(h, 2, batch=4, sb_iters=1)
+    assert full["complete"] and full["open"] == 0
+    assert sum(full["bounded_by_depth"]) == full["bounded"] and full["bounded_by_depth"][0] == 1
+    path = str(tmp_path / "d.ckpt")
+    r = pkg.qap_bnb_run(h, 2, batch=4, sb_iters=1, checkpoint_path=path, max_nodes=6)
+    assert not r["complete"] and r["open"] > 0 and r["depth_max"] >= 1
+    while not r["complete"]:
+        r = pkg.qap_bnb_run(h, 2, batch=4, sb_iters=1, checkpoint_path=path, max_nodes=6, resume=True)
+    assert r["bounded_by_depth"] == full["bounded_by_depth"] and r["open"] == 0
+    pkg.qap_destroy(h)
