@@ -142,87 +142,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
-// Argmin over the two columns of every lane by (value, matched?, column), through the full
-// order-preserving key: exact for every value (negatives, -0).  Out of line: taken only when
-// some candidate is negative.
-struct ArgMin2 {
-    int j1;
-    int free;
-    double delta;
-};
-__device__ __noinline__ ArgMin2 warp_argmin_keyed2(double m0, double m1, int p0, int p1)
-{
-    uint64_t key = okey(m0);
-    int rank = (p0 >= 0 ? 2 : 0);
-    const uint64_t k1 = okey(m1);
-    const int r1 = (p1 >= 0 ? 2 : 0) + 1;
-    if (k1 < key || (k1 == key && r1 < rank)) {
-        key = k1;
-        rank = r1;
-    }
-    const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
-    const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
-    const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
-    const bool tie = (hi == mhi) && (lo == mlo);
-    const uint32_t mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
-    const uint32_t pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
-    ArgMin2 r;
-    r.j1 = (__ffs(pick) - 1) + 32 * (static_cast<int>(mr) % 2);
-    r.free = static_cast<int>(mr) < 2;
-    r.delta = okey_inv((static_cast<uint64_t>(mhi) << 32) | mlo);
-    return r;
-}
-
-// Two columns per lane (m in (32, 64]).  While no candidate is negative (Dijkstra distances
-// are >= 0 up to rounding; settled columns hold +NaN) the raw bits order the values as signed
-// 64-bit integers: the lane-local pick compares raw bits (a negative candidate always wins it,
-// so a negative anywhere shows up as a negative minimal high word and takes the keyed path),
-// the warp-wide pick is one signed redux on the high words, and a minimum held by one lane is
-// read from it by shuffle.
-template <int CPL>
-__device__ __forceinline__ void warp_argmin(const double (&minv)[CPL], const int (&poff)[CPL], int &j1, bool &j1free,
-                                            double &delta)
-{
-    static_assert(CPL == 2, "CPL == 1 uses warp_lap_solve1; m <= 64");
-    const int64_t b0 = __double_as_longlong(minv[0]), b1 = __double_as_longlong(minv[1]);
-    const int r0 = (poff[0] >= 0 ? 2 : 0), r1 = (poff[1] >= 0 ? 2 : 0) + 1;
-    const bool p1 = b1 < b0 || (b1 == b0 && r1 < r0);
-    const int64_t kb = p1 ? b1 : b0;
-    const int rank = p1 ? r1 : r0;
-    const int32_t hs = static_cast<int32_t>(kb >> 32);
-    const uint32_t lo = static_cast<uint32_t>(kb);
-    const int32_t mhs = __reduce_min_sync(FULL_MASK, hs);
-    if (mhs < 0) {
-        const ArgMin2 r = warp_argmin_keyed2(minv[0], minv[1], poff[0], poff[1]);
-        j1 = r.j1;
-        j1free = r.free != 0;
-        delta = r.delta;
-        return;
-    }
-    const uint32_t hb = __ballot_sync(FULL_MASK, hs == mhs);
-    uint32_t mlo, mr, pick;
-    if (hb & (hb - 1u)) {  // several lanes share the minimal high word: low words, then rank
-        mlo = __reduce_min_sync(FULL_MASK, hs == mhs ? lo : 0xffffffffu);
-        const bool tie = (hs == mhs) && (lo == mlo);
-        mr = __reduce_min_sync(FULL_MASK, tie ? static_cast<uint32_t>(rank) : 0xffu);
-        pick = __ballot_sync(FULL_MASK, tie && static_cast<uint32_t>(rank) == mr);
-    } else {  // one lane holds the minimum (its lane-local pick already applied the rank)
-        const int w = __ffs(hb) - 1;
-        mlo = __shfl_sync(FULL_MASK, lo, w);
-        mr = static_cast<uint32_t>(__shfl_sync(FULL_MASK, rank, w));
-        pick = hb;
-    }
-    j1 = (__ffs(pick) - 1) + 32 * (static_cast<int>(mr) % 2);
-    j1free = static_cast<int>(mr) < 2;
-    delta = __hiloint2double(mhs, static_cast<int>(mlo));
-}
-
-template <int CPL, class T>
-__device__ __forceinline__ T sel_t(const T (&a)[CPL], int t)
-{
-    return (CPL == 1 || t == 0) ? a[0] : a[CPL - 1];
-}
-
 // Munkres' row reduction (reading R4, oracle O2): u_r = min_s M[r][s] for every row,
 // v = 0, and the initial partial assignment on the zeros this creates — row r takes the
 // lowest column attaining its minimum unless a lower row took that column.  Lane `lane`
@@ -287,140 +206,10 @@ __device__ __forceinline__ void munkres_init(const double *M, int m, int lane, c
     __syncwarp();  // the scratch is free again
 }
 
-// Solve the m×m LAP whose row-major costs start at M (shared memory): Munkres' row
-// reduction, then the rows left are inserted in ascending order, each by one
-// shortest-augmenting-path search.  Lane `lane` owns columns lane + 32 t.
-// Outputs per owned column: poff (matched row × 8m bytes), v, ucol.
-template <int CPL, bool COUNT>
-__device__ __forceinline__ void warp_lap_solve(const double *M, int m, int lane, int *scratch, int (&poff)[CPL],
-                                               double (&v)[CPL], double (&ucol)[CPL], int &steps)
-{
-    const double *Mlane = M + lane;
-    double minv[CPL];
-    int way[CPL];
-    const int rowb = m * 8;
-    int col[CPL];
-#pragma unroll
-    for (int t = 0; t < CPL; t++) {
-        v[t] = 0.0;
-        way[t] = -1;
-        col[t] = lane + 32 * t;
-    }
-    double rmin[CPL];
-    uint32_t rmask[CPL];
-    munkres_init<CPL>(M, m, lane, col, scratch, poff, ucol, rmin, rmask);
-    // the rows the row reduction left unmatched, ascending (P:205 Hungarian, one augmentation
-    // per row)
-    uint64_t um = ~static_cast<uint64_t>(rmask[0]);
-    if (CPL > 1) um &= ~(static_cast<uint64_t>(rmask[CPL - 1]) << 32);
-    if (m < 64) um &= (1ull << m) - 1ull;
-    for (; um; um &= um - 1ull) {
-        const int i = __ffsll(static_cast<long long>(um)) - 1;
-        // u of row i = u[p[dummy]]: its row minimum.  Dijkstra from row i with absolute
-        // tentative distances (minv); the scanned row i0 enters as c = dist(its column) -
-        // u[i0]; the potentials move once, after the search (as warp_lap_solve1).
-        const double ui = __shfl_sync(FULL_MASK, sel_t<CPL>(rmin, i >> 5), i & 31);
-        uint32_t dhi[CPL];  // settled: high word of the column's distance (low word stays in minv)
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            minv[t] = (lane + 32 * t) < m ? CUDART_INF : qnan();
-            dhi[t] = 0xffffffffu;
-        }
-        int j0 = -1, i0off = i * rowb;
-        double c = 0.0 - ui, dfin;
-        int jfree;
-        while (true) {
-            const double *row = reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off);
-#pragma unroll
-            for (int t = 0; t < CPL; t++) {
-                const double cur = (row[32 * t] - v[t]) + c;
-                if (cur < minv[t]) {  // false for settled columns (minv = NaN)
-                    minv[t] = cur;
-                    way[t] = j0;
-                }
-            }
-            int j1;
-            bool j1free;
-            double delta;  // minv of column j1: its distance
-            warp_argmin<CPL>(minv, poff, j1, j1free, delta);
-            // next row to scan (used only if j1 is matched): its offset and u
-            const int src = j1 & 31, tt = j1 >> 5;
-            const int nx_off = __shfl_sync(FULL_MASK, sel_t<CPL>(poff, tt), src);
-            const double nx_u = __shfl_sync(FULL_MASK, sel_t<CPL>(ucol, tt), src);
-#pragma unroll
-            for (int t = 0; t < CPL; t++) {
-                if (lane + 32 * t == j1) {  // settle column j1
-                    dhi[t] = static_cast<uint32_t>(__double2hiint(minv[t]));
-                    minv[t] = __hiloint2double(0x7ff80000, __double2loint(minv[t]));
-                }
-            }
-            if (COUNT) steps++;
-            if (j1free) {
-                jfree = j1;
-                dfin = delta;
-                break;
-            }
-            i0off = nx_off;
-            c = delta - nx_u;
-            j0 = j1;
-        }
-        // potentials: every column settled in this search moves by dfin - dist (the free end
-        // column by +0); row i's u by dfin
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            if (dhi[t] != 0xffffffffu) {
-                const double tt = dfin - __hiloint2double(static_cast<int>(dhi[t]), __double2loint(minv[t]));
-                ucol[t] = ucol[t] + tt;
-                v[t] = v[t] - tt;
-            }
-        }
-        const double ucur = ui + dfin;
-        // augment along way[]: columns on the path take the row (and its u) of way[c].
-        // The path (a few columns) is walked once with warp-uniform values; its columns are
-        // collected in a bit mask per column group t.
-        uint32_t onmask[CPL];
-#pragma unroll
-        for (int t = 0; t < CPL; t++) onmask[t] = 0u;
-        for (int c = jfree; c >= 0;) {
-            const int src = c & 31, tt = c >> 5;
-#pragma unroll
-            for (int t = 0; t < CPL; t++)
-                if (t == tt) onmask[t] |= 1u << src;
-            c = __shfl_sync(FULL_MASK, sel_t<CPL>(way, tt), src);
-        }
-        int pold[CPL];
-        double uold[CPL];
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            pold[t] = poff[t];
-            uold[t] = ucol[t];
-        }
-#pragma unroll
-        for (int t = 0; t < CPL; t++) {
-            const int w = way[t];
-            const int wl = w & 31, wt = w >> 5;  // w < 0 (dummy): values unused below
-            int np = i * rowb;
-            double nu = ucur;
-#pragma unroll
-            for (int s = 0; s < CPL; s++) {
-                const int sp = __shfl_sync(FULL_MASK, pold[s], wl);
-                const double su = __shfl_sync(FULL_MASK, uold[s], wl);
-                if (w >= 0 && wt == s) {
-                    np = sp;
-                    nu = su;
-                }
-            }
-            if ((onmask[t] >> lane) & 1u) {
-                poff[t] = np;
-                ucol[t] = nu;
-            }
-        }
-    }
-}
-
-// One column per lane (m <= 32): the same algorithm and the same floating-point
-// operations as warp_lap_solve<CPL>, with column c held by lane 31 - c (Mlane points at the
-// lane's column), so that "lowest column index" is the highest set lane bit (one FLO).  The
+// One column per lane (m <= 32): Munkres' row reduction (munkres_init), then the rows left are
+// inserted in ascending order, each by one shortest-augmenting-path search (Dijkstra with
+// absolute tentative distances; the potentials move once, after the search).  Column c is
+// held by lane 31 - c, so that "lowest column index" is the highest set lane bit (one FLO).  The
 // argmin takes the order key's high word first (the low word only on ties, a warp-uniform
 // branch), then prefers a free column (a lane mask updated once per augmentation), then
 // the lowest column; way[] and the augmenting path (one lane mask) are in lane ids.
@@ -502,10 +291,10 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
             const uint32_t ft = bal & freemask;
             const double nc = __shfl_sync(FULL_MASK, cj, j1);
             const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
-            if (lane == j1) {  // settle column j1: keep its distance's high word, NaN in minv
-                dhi = static_cast<uint32_t>(__double2hiint(minv));
-                minv = __hiloint2double(0x7ff80000, __double2loint(minv));
-            }
+            // settle column j1: keep its distance's high word, NaN in minv (selects)
+            const bool me = lane == j1;
+            dhi = me ? static_cast<uint32_t>(__double2hiint(minv)) : dhi;
+            minv = __hiloint2double(me ? 0x7ff80000 : __double2hiint(minv), __double2loint(minv));
             if (COUNT) steps++;
             if (ft) break;
             i0off = nx_off;
@@ -530,6 +319,136 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
         if ((onmask >> lane) & 1u) {
             poff = way >= 0 ? sp : i * rowb;
             ucol = way >= 0 ? su : ucur;
+        }
+    }
+}
+
+// Two columns per lane (32 < m <= 64): column 32 t + 31 - lane in slot t (the one-column
+// solver's reversed order, so the lowest column of a slot is the highest lane: one bfind).
+// The same algorithm and floating-point operations as warp_lap_solve1.  Argmin on the common
+// path: one signed redux per slot on the raw fp64 high words (non-negative values order as
+// signed integers, settled columns hold +NaN); when the two slot minima differ and one lane
+// holds the smaller, that lane's column is the minimum; every other case (equal high words,
+// a negative value) takes argmin2_keyed, the full (value, matched?, column) order.
+__device__ __noinline__ int argmin2_keyed(double m0, double m1, int p0, int p1, int lane)
+{
+    const uint64_t k0 = okey(m0), k1 = okey(m1);
+    const int r0 = p0 >= 0 ? 1 : 0, r1 = p1 >= 0 ? 1 : 0;
+    // slot 0 holds the lower column, so it wins equal (key, matched?)
+    const bool s1 = k1 < k0 || (k1 == k0 && r1 < r0);
+    const uint64_t key = s1 ? k1 : k0;
+    const uint32_t rank = static_cast<uint32_t>(s1 ? r1 : r0);
+    const uint32_t col = static_cast<uint32_t>((s1 ? 63 : 31) - lane);
+    const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
+    const uint32_t mhi = __reduce_min_sync(FULL_MASK, hi);
+    const uint32_t mlo = __reduce_min_sync(FULL_MASK, hi == mhi ? lo : 0xffffffffu);
+    const bool tie = hi == mhi && lo == mlo;
+    const uint32_t mr = __reduce_min_sync(FULL_MASK, tie ? rank : 0xffu);
+    return static_cast<int>(__reduce_min_sync(FULL_MASK, (tie && rank == mr) ? col : 0xffu));
+}
+template <bool COUNT>
+__device__ __forceinline__ void warp_lap_solve2(const double *M, int m, int lane, int *scratch, int (&poff)[2],
+                                                double (&v)[2], double (&ucol)[2], int &steps)
+{
+    const double *Mlane = M + (31 - lane);  // slot 0; slot 1 is 32 doubles further
+    const int rowb = m * 8;
+    v[0] = v[1] = 0.0;
+    int way0 = -1, way1 = -1;  // predecessor column of each owned column
+    const double minv00 = CUDART_INF, minv01 = 63 - lane < m ? CUDART_INF : qnan();
+    int col[2] = {31 - lane, 63 - lane};
+    double rm[2];
+    uint32_t rmask[2];
+    munkres_init<2>(M, m, lane, col, scratch, poff, ucol, rm, rmask);
+    uint64_t um = ~(static_cast<uint64_t>(rmask[0]) | (static_cast<uint64_t>(rmask[1]) << 32));
+    if (m < 64) um &= (1ull << m) - 1ull;
+    // the rows the row reduction left unmatched, ascending (P:205 Hungarian, one augmentation
+    // per row)
+    for (; um; um &= um - 1ull) {
+        const int i = __ffsll(static_cast<long long>(um)) - 1;
+        const double ui = __shfl_sync(FULL_MASK, i < 32 ? rm[0] : rm[1], i & 31);
+        double minv0 = minv00, minv1 = minv01, c = 0.0 - ui;
+        uint32_t dhi0 = 0xffffffffu, dhi1 = 0xffffffffu;
+        int j0 = -1, i0off = i * rowb, jcol, jl, jt;
+#pragma unroll 2
+        for (;;) {
+            const double *row = reinterpret_cast<const double *>(reinterpret_cast<const char *>(Mlane) + i0off);
+            const double cur0 = (row[0] - v[0]) + c, cur1 = (row[32] - v[1]) + c;
+            if (cur0 < minv0) {  // false for settled columns (minv = NaN)
+                minv0 = cur0;
+                way0 = j0;
+            }
+            if (cur1 < minv1) {
+                minv1 = cur1;
+                way1 = j0;
+            }
+            const double cj0 = minv0 - ucol[0], cj1 = minv1 - ucol[1];  // dist - u of the column's row
+            const int32_t hs0 = __double2hiint(minv0), hs1 = __double2hiint(minv1);
+            const int32_t m0 = __reduce_min_sync(FULL_MASK, hs0), m1 = __reduce_min_sync(FULL_MASK, hs1);
+            bool uniq = false;
+            if (m0 >= 0 && m1 >= 0 && m0 != m1) {
+                const bool t1 = m1 < m0;
+                const uint32_t bal = __ballot_sync(FULL_MASK, (t1 ? hs1 : hs0) == (t1 ? m1 : m0));
+                if (!(bal & (bal - 1u))) {
+                    jcol = (t1 ? 63 : 31) - hibit(bal);
+                    uniq = true;
+                }
+            }
+            if (!uniq) jcol = argmin2_keyed(minv0, minv1, poff[0], poff[1], lane);
+            jt = jcol >> 5;
+            jl = 31 - (jcol & 31);
+            const int nx_off = __shfl_sync(FULL_MASK, jt ? poff[1] : poff[0], jl);
+            const double nc = __shfl_sync(FULL_MASK, jt ? cj1 : cj0, jl);
+            // settle column jcol: keep its distance's high word, NaN in minv (selects, no branch)
+            const bool me0 = lane == jl && jt == 0, me1 = lane == jl && jt != 0;
+            dhi0 = me0 ? static_cast<uint32_t>(__double2hiint(minv0)) : dhi0;
+            dhi1 = me1 ? static_cast<uint32_t>(__double2hiint(minv1)) : dhi1;
+            minv0 = __hiloint2double(me0 ? 0x7ff80000 : __double2hiint(minv0), __double2loint(minv0));
+            minv1 = __hiloint2double(me1 ? 0x7ff80000 : __double2hiint(minv1), __double2loint(minv1));
+            if (COUNT) steps++;
+            if (nx_off < 0) break;  // a free column: the augmenting path ends here
+            i0off = nx_off;
+            c = nc;
+            j0 = jcol;
+        }
+        // potentials: every column settled in this search moves by dfin - dist (the free end
+        // column by +0); row i's u by dfin
+        const double d0 = __hiloint2double(static_cast<int>(dhi0), __double2loint(minv0)),
+                     d1 = __hiloint2double(static_cast<int>(dhi1), __double2loint(minv1));
+        const double dfin = __shfl_sync(FULL_MASK, jt ? d1 : d0, jl);
+        if (dhi0 != 0xffffffffu) {
+            const double tt = dfin - d0;
+            ucol[0] = ucol[0] + tt;
+            v[0] = v[0] - tt;
+        }
+        if (dhi1 != 0xffffffffu) {
+            const double tt = dfin - d1;
+            ucol[1] = ucol[1] + tt;
+            v[1] = v[1] - tt;
+        }
+        const double ucur = ui + dfin;
+        // augment along way[]: columns on the path take the row (and its u) of their
+        // predecessor column; the path is walked once with warp-uniform values
+        uint32_t on0 = 0u, on1 = 0u;
+        for (int cc = jcol; cc >= 0;) {
+            const int cl = 31 - (cc & 31);
+            if (cc >> 5) on1 |= 1u << cl;
+            else on0 |= 1u << cl;
+            cc = __shfl_sync(FULL_MASK, (cc >> 5) ? way1 : way0, cl);
+        }
+        const int po0 = poff[0], po1 = poff[1];
+        const double uo0 = ucol[0], uo1 = ucol[1];
+#pragma unroll
+        for (int t = 0; t < 2; t++) {
+            const int w = t ? way1 : way0;
+            const int wl = 31 - (w & 31);  // w < 0 (the inserted row): values unused below
+            const int sp0 = __shfl_sync(FULL_MASK, po0, wl), sp1 = __shfl_sync(FULL_MASK, po1, wl);
+            const double su0 = __shfl_sync(FULL_MASK, uo0, wl), su1 = __shfl_sync(FULL_MASK, uo1, wl);
+            const int np = w < 0 ? i * rowb : ((w >> 5) ? sp1 : sp0);
+            const double nu = w < 0 ? ucur : ((w >> 5) ? su1 : su0);
+            if ((((t ? on1 : on0) >> lane) & 1u)) {
+                poff[t] = np;
+                ucol[t] = nu;
+            }
         }
     }
 }
@@ -683,7 +602,7 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
     extern __shared__ __align__(128) unsigned char smem[];
     const int wpc = blockDim.x >> 5, warp = __shfl_sync(FULL_MASK, (int)(threadIdx.x >> 5), 0),
               lane = threadIdx.x & 31;
-    const int col0 = CPL == 1 ? 31 - lane : lane;  // this lane's (first) column
+    const int col0 = 31 - lane;  // this lane's column in slot 0 (slot t: col0 + 32 t)
     const int m = a.m;
     const size_t bufb = lap_buf_bytes(m, CPL);
     unsigned char *wbase = smem + (size_t)warp * lap_warp_smem(m, CPL);
@@ -744,8 +663,8 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
             if (a.lvl == LAP_BATCH) warp_lap_solve1<true>(M, m, lane, scratch, poff[0], v[0], ucol[0], steps);
             else warp_lap_solve1<false>(M, m, lane, scratch, poff[0], v[0], ucol[0], steps);
         } else {
-            if (a.lvl == LAP_BATCH) warp_lap_solve<CPL, true>(M, m, lane, scratch, poff, v, ucol, steps);
-            else warp_lap_solve<CPL, false>(M, m, lane, scratch, poff, v, ucol, steps);
+            if (a.lvl == LAP_BATCH) warp_lap_solve2<true>(M, m, lane, scratch, poff, v, ucol, steps);
+            else warp_lap_solve2<false>(M, m, lane, scratch, poff, v, ucol, steps);
         }
         bool bad;
         const double *Mg = a.src + b * a.ld;

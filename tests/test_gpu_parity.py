@@ -345,6 +345,33 @@ def test_wide_columns_level2_n35(orc, torch, pkg):
     pkg.qap_destroy(h)
 
 
+def test_config5_n40_one_iteration(orc, torch, pkg):
+    """BASELINE config 5's size, N = 40 (tai40b-shaped; level-2 LAPs of m = 38 with two
+    columns per lane, 1,216,800 of them, D = 14 GB): one iteration against the oracle run
+    live on all host cores (bit-identical to one thread) — GLB exact; LB, all of B and C and
+    the whole of D within 1e-9 (chunked comparison)."""
+    import os
+    inst = qapgen.taib(40, 1)
+    h = pkg.qap_rlt2_create(40, inst.F, inst.D)
+    g = pkg.qap_rlt2_bound(h, 1, trace=True)
+    B, C, D, lb = gpu_state(pkg, h, 40)
+    pkg.qap_destroy(h)
+    orc.set_threads(os.cpu_count() or 1)
+    try:
+        st = orc.State(inst.F, inst.D)
+        o = st.bound(1, trace=True)
+    finally:
+        orc.set_threads(1)
+    assert g["lb_glb"] == o["lb_glb"] == de.gilmore_lawler(inst.F, inst.D)
+    rel_close(g["trace"], o["trace"])
+    rel_close(B, st.B)
+    rel_close(C, st.C)
+    Dref = st.D
+    D = D.reshape(Dref.shape)
+    for a in range(0, Dref.shape[0], 65536):
+        rel_close(D[a:a + 65536], Dref[a:a + 65536])
+
+
 def test_bound_async_concurrent(torch, pkg):
     """Independent bounds on several handles, enqueued before any is read back."""
     inst = qapgen.taib(10, 6)
