@@ -291,10 +291,10 @@ __device__ __forceinline__ void warp_lap_solve1(const double *M, int m, int lane
             const uint32_t ft = bal & freemask;
             const double nc = __shfl_sync(FULL_MASK, cj, j1);
             const int nx_off = __shfl_sync(FULL_MASK, poff, j1);
-            // settle column j1: keep its distance's high word, NaN in minv (selects)
-            const bool me = lane == j1;
-            dhi = me ? static_cast<uint32_t>(__double2hiint(minv)) : dhi;
-            minv = __hiloint2double(me ? 0x7ff80000 : __double2hiint(minv), __double2loint(minv));
+            if (lane == j1) {  // settle column j1: keep its distance's high word, NaN in minv
+                dhi = static_cast<uint32_t>(__double2hiint(minv));
+                minv = __hiloint2double(0x7ff80000, __double2loint(minv));
+            }
             if (COUNT) steps++;
             if (ft) break;
             i0off = nx_off;
