@@ -397,13 +397,15 @@ def main():
         hb = pkg.qap_rlt2_create(20, bi.F, bi.D, device=local_rank, stream=stream.cuda_stream)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r20 = pkg.qap_bnb_run(hb, BNB_ITERS, batch=20, sb_iters=1)
+        r20 = pkg.qap_bnb_run(hb, 60, K=1e-4, batch=20, sb_iters=1, warm=True)
         torch.cuda.synchronize()
         dt20 = time.perf_counter() - t0
         pkg.qap_destroy(hb)
         assert r20["complete"] and bi.evaluate([int(x) for x in r20["perm"]]) == r20["opt"]
-        bnb20 = {"config": f"tai20b-shaped seed {SEED}, full B&B, {BNB_ITERS} RLT2 iterations per node, strong "
-                           "branching (RLT1, 1 iteration), children bounded 20 at a time, UB0=inf",
+        bnb20 = {"config": f"tai20b-shaped seed {SEED}, full B&B to proven optimality: up to 60 RLT2 iterations "
+                           "per node with the progress stop K = 1e-4 (P:183, R14), warm children (folded from the "
+                           "parent, R31), strong branching (RLT1, 1 iteration, P:254), children bounded 20 at a "
+                           "time, UB0=inf",
                  "opt": r20["opt"], "bounded_nodes": r20["bounded"], "leaves": r20["leaves"],
                  "pruned": r20["pruned"], "cut_by_rlt1": r20["sb_cut"], "seconds": dt20,
                  "nodes_per_s": r20["bounded"] / dt20, "bounded_by_depth": r20["bounded_by_depth"],

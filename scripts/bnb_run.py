@@ -82,6 +82,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=200)
     ap.add_argument("--budget-s", type=float, default=600)
     ap.add_argument("--ckpt", default=None)
+    ap.add_argument("--resume", action="store_true",
+                    help="continue the search in --ckpt (time and counters carry over via <ckpt>.json)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
 
@@ -92,8 +94,15 @@ def main():
     inst = qapgen.make(a.family, a.n, a.seed)
     h = pkg.qap_rlt2_create(a.n, inst.F, inst.D, device=0)
     ckpt = a.ckpt or f"/tmp/bnb_{a.family}{a.n}_s{a.seed}.ckpt"
-    if os.path.exists(ckpt):
-        os.remove(ckpt)
+    side = ckpt + ".json"
+    carried = 0.0
+    if a.resume and os.path.exists(ckpt):
+        carried = json.load(open(side))["seconds"] if os.path.exists(side) else 0.0
+    else:
+        a.resume = False
+        for f in (ckpt, side):
+            if os.path.exists(f):
+                os.remove(f)
     out = open(a.out, "a") if a.out else None
     cfg = {"instance": f"{a.family}{a.n}-shaped seed {a.seed}", "N": a.n, "iters_per_node": a.iters,
            "strong_branching": a.sb, "warm_children": a.warm, "batch": a.batch or a.n, "UB0": a.ub0, "K": a.K}
@@ -105,9 +114,10 @@ def main():
             out.write(line + "\n")
             out.flush()
 
-    emit({"config": cfg})
-    t0 = time.perf_counter()
-    first, r, last_b, last_t = True, None, 0, t0
+    emit({"config": cfg, "resumed_from_s": carried if a.resume else None})
+    t0 = time.perf_counter() - carried
+    t_call = time.perf_counter()
+    first, r, last_b, last_t = not a.resume, None, (None if a.resume else 0), t_call
     while True:
         r = pkg.qap_bnb_run(h, a.iters, K=a.K, UB0=a.ub0, batch=a.batch or a.n, sb_iters=a.sb, warm=a.warm,
                             checkpoint_path=ckpt, max_nodes=a.chunk, resume=not first)
@@ -115,14 +125,15 @@ def main():
         torch.cuda.synchronize()
         now = time.perf_counter()
         el = now - t0
+        json.dump({"seconds": el}, open(side, "w"))
         prog = 1.0 if r["complete"] else progress(read_checkpoint(ckpt))
         emit({"elapsed_s": el, "bounded": r["bounded"], "leaves": r["leaves"], "pruned": r["pruned"],
               "sb_cut": r["sb_cut"], "open": r["open"], "depth": r["depth_max"], "opt": r["opt"],
-              "nodes_per_s_chunk": (r["bounded"] - last_b) / max(1e-9, now - last_t),
+              "nodes_per_s_chunk": None if last_b is None else (r["bounded"] - last_b) / max(1e-9, now - last_t),
               "progress": prog, "projected_total_s": el / prog if prog > 0 else None,
               "bounded_by_depth": r["bounded_by_depth"], "complete": r["complete"]})
         last_b, last_t = r["bounded"], now
-        if r["complete"] or el > a.budget_s:
+        if r["complete"] or now - t_call > a.budget_s:
             break
     el = time.perf_counter() - t0
     opt_ok = None

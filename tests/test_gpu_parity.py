@@ -495,3 +495,22 @@ def test_bnb_depth_counters_and_open(torch, pkg, tmp_path):
         r = pkg.qap_bnb_run(h, 2, batch=4, sb_iters=1, checkpoint_path=path, max_nodes=6, resume=True)
     assert r["bounded_by_depth"] == full["bounded_by_depth"] and r["open"] == 0
     pkg.qap_destroy(h)
+
+
+def test_largest_sizes(torch, pkg):
+    """Maximum sizes: N = 50 (D = 110 GB of the 180 GB, level-2 LAPs of m = 48 with two columns
+    per lane) bounds on one B200 — iteration 0 equals the closed-form Gilmore–Lawler bound and
+    the LB rises monotonically; N = 64 (the ABI's maximum, D = 250 GB) is refused with
+    QAP_E_CAPACITY and a message, leaving nothing allocated."""
+    inst = qapgen.taib(50, 1)
+    h = pkg.qap_rlt2_create(50, inst.F, inst.D)
+    g = pkg.qap_rlt2_bound(h, 2, trace=True)
+    pkg.qap_destroy(h)
+    assert g["lb_glb"] == de.gilmore_lawler(inst.F, inst.D)
+    tr = np.concatenate([[g["lb_glb"]], g["trace"]])
+    assert (np.diff(tr) >= 0).all() and g["iters"] == 2
+    big = qapgen.taib(64, 1)
+    with pytest.raises(pkg.QapError) as e:
+        pkg.qap_rlt2_create(64, big.F, big.D)
+    assert e.value.status == pkg.QAP_E_CAPACITY and "GB" in str(e.value)
+    torch.cuda.synchronize()
