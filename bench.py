@@ -107,14 +107,16 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profiled_traffic(kernel, key="dram_bytes_per_launch"):
+def profiled_traffic(kernel, key="dram_bytes_per_launch", n=30, sharded=False):
     """Per-launch figure (dram read+write bytes, warp instructions) of the committed ncu
-    --set full summary, if any."""
+    --set full summary, if any — only for the workload it was captured on (its "n", one
+    unsharded bound): another size's launch moves other bytes."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(p):
-        d = json.load(open(p))
-        if kernel in d:
-            return d[kernel].get(key)
+    if sharded or not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    if kernel in d and int(d[kernel].get("n", 30)) == n:
+        return d[kernel].get(key)
     return None
 
 
@@ -468,8 +470,8 @@ def main():
              "transfer": "k_transfer_tma" if n >= 10 and not sharded else "k_transfer"}
     roof = {"bound": "hbm", "kernel": names[dom],
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": profiled_traffic(dom), "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
-    ins = profiled_traffic(dom, "inst_executed_per_launch")
+            "traffic": profiled_traffic(dom, n=n, sharded=sharded), "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src}
+    ins = profiled_traffic(dom, "inst_executed_per_launch", n, sharded)
     if ins:  # what actually bounds the LAP kernel: warp-instruction issue
         sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
         mhz = clk.summary().get("sm_mhz") or 1965.0
@@ -484,14 +486,15 @@ def main():
     if other in per:  # the other D kernel against the same roofline (the transfer is HBM-bound)
         a2 = alg_bytes / (per[other]["avg_ms"] / 1e3) / 1e9
         roof["other_kernel"] = {"kernel": names[other], "achieved": a2, "frac": a2 / peak,
-                                "traffic": profiled_traffic(other)}
+                                "traffic": profiled_traffic(other, n=n, sharded=sharded)}
     iter_ms = (per["sigma"]["avg_ms"] + per.get("transfer", {"avg_ms": 0.0})["avg_ms"] + per["lap2"]["avg_ms"]
                + per["lap1"]["avg_ms"] * T / (T + 1) + per["lap0"]["avg_ms"])
     # the whole iteration against the same roofline (both bandwidth readings)
     wall_iter_ms = ms / (T * args.steps)              # production path, incl. init + iteration 0 share
     dram_iter = None
-    if profiled_traffic("transfer") and profiled_traffic("lap2"):
-        dram_iter = profiled_traffic("transfer") + profiled_traffic("lap2")
+    tt, tl = profiled_traffic("transfer", n=n, sharded=sharded), profiled_traffic("lap2", n=n, sharded=sharded)
+    if tt and tl:
+        dram_iter = tt + tl
     roof["iteration"] = {
         "alg_bytes": alg_bytes, "ms": wall_iter_ms, "kernel_ms": iter_ms,
         "effective_GBps": alg_bytes / (wall_iter_ms / 1e3) / 1e9,

@@ -70,6 +70,9 @@ struct qap_rlt2 {
     bool loopback = false;    // member of an in-process group: the group driver moves data
     ShardPlan plan;           // for the current n
     int *dTiles = nullptr, *dTinfo = nullptr;
+    // the transfer of the local tiles runs on sSide while the shared tiles are exchanged
+    cudaStream_t sSide = nullptr;
+    cudaEvent_t evFork = nullptr, evLocal = nullptr;
     size_t tiles_cap = 0, slots_cap = 0;
     int64_t dblk_cap = 0;     // stored blocks the D allocation can hold
     double *dSend = nullptr, *dRecv = nullptr, *dSall = nullptr;
@@ -184,6 +187,9 @@ static void free_all(qap_rlt2 *h)
     if (h->sCap) cudaStreamDestroy(h->sCap);
     cudaFree(h->dTiles);
     cudaFree(h->dTinfo);
+    if (h->evFork) cudaEventDestroy(h->evFork);
+    if (h->evLocal) cudaEventDestroy(h->evLocal);
+    if (h->sSide) cudaStreamDestroy(h->sSide);
     cudaFree(h->dSend);
     cudaFree(h->dRecv);
     cudaFree(h->dSall);
@@ -315,7 +321,7 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
     ALLOC(h->dSigma, bytesS);
     ALLOC(h->dTrace, (size_t)h->trace_cap * 8);
     ALLOC(h->dCtl, sizeof(Ctl));
-    ALLOC(h->dTriples, (size_t)gN.n * (gN.n - 1) * (gN.n - 2) / 6 * sizeof(int) + 16);
+    ALLOC(h->dTriples, (size_t)gN.n * (gN.n - 1) * (gN.n - 2) / 6 * 2 * sizeof(int) + 16);  // two orders (write_triples)
     ALLOC(h->dSched, sizeof(Sched));
     if (world > 1) {
         ALLOC(h->dTiles, h->tiles_cap * sizeof(int) + 16);
@@ -323,6 +329,13 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         ALLOC(h->dSend, h->slots_cap * kSlot * 8 + 16);
         ALLOC(h->dRecv, h->slots_cap * kSlot * 8 + 16);
         ALLOC(h->dSall, (size_t)gN.nblk * 8 + 16);
+        if ((e = cudaStreamCreateWithFlags(&h->sSide, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&h->evFork, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&h->evLocal, cudaEventDisableTiming)) != cudaSuccess) {
+            free_all(h);
+            delete h;
+            return cuda_fail(nullptr, e, "side stream");
+        }
         if (!loopback && opts->host_transport) {
             h->tp = make_host_transport(*opts->host_transport, world, rank);
         } else if (!loopback) {
@@ -540,17 +553,33 @@ static cudaError_t run_shard_sub(qap_rlt2 *h, int phase, int sub, cudaStream_t s
     cudaError_t e = cudaSuccess;
     const Geom &g = h->geom;
     const ShardPlan &P = h->plan;
+    // the plan lists the local tiles first, then the shared ones (make_plan)
+    const int nloc = P.n_local, nsh = (int)P.tiles.size() - P.n_local;
     if (phase == QAP_PHASE_TRANSFER && sub == 0) {
         e = launch(h, QAP_K_SIGMA, st, [&](cudaStream_t s) {
             return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->dSched, s);
         });
         if (e) return e;
         TransferArgs A = transfer_args(h);
-        A.pack = 1;
-        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, (int)P.tiles.size(), s); });
+        A.pack = 1;  // pass 1: this side's partials of the shared tiles
+        A.tiles += nloc;
+        A.tinfo += nloc;
+        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, nsh, s); });
+        if (e || nloc == 0) return e;
+        // the local tiles need no exchange: transferred on the side stream while the caller
+        // exchanges the shared tiles' partials on `st` (joined in sub-phase 1); disjoint classes
+        if ((e = cudaEventRecord(h->evFork, st)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(h->sSide, h->evFork, 0)) != cudaSuccess)
+            return e;
+        TransferArgs L = transfer_args(h);
+        e = launch(h, QAP_K_TRANSFER, h->sSide, [&](cudaStream_t s) { return launch_transfer(L, nloc, s); });
+        if (e == cudaSuccess) e = cudaEventRecord(h->evLocal, h->sSide);
     } else if (phase == QAP_PHASE_TRANSFER && sub == 1) {
-        TransferArgs A = transfer_args(h);
-        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, (int)P.tiles.size(), s); });
+        if (nloc > 0 && (e = cudaStreamWaitEvent(st, h->evLocal, 0)) != cudaSuccess) return e;
+        TransferArgs A = transfer_args(h);  // pass 2: the class means of the shared tiles
+        A.tiles += nloc;
+        A.tinfo += nloc;
+        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, nsh, s); });
         h->d_zero = 0;
         h->b_zero = h->c_zero = 1;
     } else if (phase == QAP_PHASE_CONC_D && sub == 0) {
@@ -1367,7 +1396,7 @@ qap_status Bnb::copy_state(qap_rlt2 *dst, const qap_rlt2 *src)
          (e = cudaMemcpyAsync(dst->dD, src->dD, nd, cudaMemcpyDeviceToDevice, dst->stream)) != cudaSuccess) ||
         (e = cudaMemcpyAsync(dst->dCtl, src->dCtl, sizeof(Ctl), cudaMemcpyDeviceToDevice, dst->stream)) !=
             cudaSuccess ||
-        (e = cudaMemcpyAsync(dst->dTriples, src->dTriples, (size_t)g.n * (g.n - 1) * (g.n - 2) / 6 * sizeof(int),
+        (e = cudaMemcpyAsync(dst->dTriples, src->dTriples, (size_t)g.n * (g.n - 1) * (g.n - 2) / 6 * 2 * sizeof(int),
                              cudaMemcpyDeviceToDevice, dst->stream)) != cudaSuccess)
         return cuda_fail(dst, e, "state copy");
     if ((e = cudaEventRecord(dst->evJoin, dst->stream)) != cudaSuccess ||

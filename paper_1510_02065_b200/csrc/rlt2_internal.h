@@ -110,6 +110,9 @@ cudaError_t launch_ctl_begin(Ctl *ctl, double K, double UB, int trace_cap, cudaS
 cudaError_t launch_sigma(const Geom &g, const double *B, const double *C, double *sigma,
                          const Ctl *ctl, Sched *sched, cudaStream_t st);
 constexpr int TT = 8;  // transfer tile edge (locations j, l, q)
+// edge of the facility-triple cubes of the TMA transfer's dispatch order (write_triples):
+// 1.18 -> 1.13-1.15 ms at N = 30 for edges 2..10 (lexicographic order: 1.18-1.20; one box)
+constexpr int kTxCube = 8;
 
 struct TransferArgs {
     Geom g;

@@ -765,10 +765,25 @@ __global__ void __launch_bounds__(1024) k_lap(const LapArgs a)
 // k_init — O0/O1: b0 with the fixed-free folds, c_ij[kl] = f'_ik d'_jl,
 // kappa; D is NOT written (the next transfer reads it as zero).
 // ---------------------------------------------------------------------------------------
-// facility triples i<k<p in lexicographic order (the transfer kernel's grid.y)
+__device__ __forceinline__ int tx_c2(int a) { return a * (a - 1) / 2; }
+__device__ __forceinline__ int tx_c3(int a) { return a * (a - 1) * (a - 2) / 6; }
+// triples (i<k<p) of the cube (a, b, c) of edge e (a <= b <= c), node size n
+__device__ __forceinline__ int tx_cube_count(int a, int b, int c, int e, int n)
+{
+    const int sa = min(e, n - a * e), sb = min(e, n - b * e), sc = min(e, n - c * e);
+    if (a == b && b == c) return tx_c3(sa);
+    if (a == b) return tx_c2(sa) * sc;
+    if (b == c) return sa * tx_c2(sb);
+    return sa * sb * sc;
+}
+// facility triples i<k<p: triples[0, ntri) in lexicographic order (the register transfer's
+// grid.y and the sharded tile ids), triples[ntri, 2 ntri) grouped into cubes of edge
+// kTxCube in (i,k,p) (cubes lexicographic, triples lexicographic within a cube): the TMA
+// transfer's dispatch order, so that the CTAs in flight read runs of neighbouring rows of the
+// same blocks in all three member views
 __device__ void write_triples(int n, int *triples)
 {
-    const int ntri = n * (n - 1) * (n - 2) / 6;
+    const int ntri = n * (n - 1) * (n - 2) / 6, e = kTxCube, nc = (n + e - 1) / e;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntri; t += gridDim.x * blockDim.x) {
         int rem = t, i = 0;
         while (rem >= (n - 1 - i) * (n - 2 - i) / 2) {
@@ -780,7 +795,20 @@ __device__ void write_triples(int n, int *triples)
             rem -= n - 1 - k;
             k++;
         }
-        triples[t] = i | (k << 8) | ((k + 1 + rem) << 16);
+        const int p = k + 1 + rem;
+        const int packed = i | (k << 8) | (p << 16);
+        triples[t] = packed;
+        const int ci = i / e, ck = k / e, cp = p / e;
+        int pos = 0;
+        for (int a = 0; a < nc; a++)
+            for (int b = a; b < nc; b++)
+                for (int c = b; c < nc; c++)
+                    if (a < ci || (a == ci && (b < ck || (b == ck && c < cp)))) pos += tx_cube_count(a, b, c, e, n);
+        for (int x = ci * e; x < min(n, ci * e + e); x++)
+            for (int y = max(x + 1, ck * e); y < min(n, ck * e + e); y++)
+                for (int z = max(y + 1, cp * e); z < min(n, cp * e + e); z++)
+                    if (x < i || (x == i && (y < k || (y == k && z < p)))) pos++;
+        triples[ntri + pos] = packed;
     }
 }
 
@@ -1413,6 +1441,7 @@ cudaError_t launch_transfer_tma(const TransferArgs &A, const TmaMaps &M, cudaStr
     if (A.ntile > 8 || ntri > 65535) return cudaErrorInvalidValue;  // n <= kMaxN = 64
     TransferArgs B = A;
     B.ntile_mul = (65536u + (unsigned)A.ntile - 1u) / (unsigned)A.ntile;  // exact y / ntile for y < 64
+    B.triples = A.triples + ntri;  // the cube-blocked dispatch order (write_triples)
     dim3 grid(A.ntile, A.ntile * A.ntile, ntri);
     const bool wide = (int64_t)A.g.nblk * A.g.ld2 >= (int64_t(1) << 32);
     constexpr int NT = 128;  // means in the boxes, 11 CTAs per SM

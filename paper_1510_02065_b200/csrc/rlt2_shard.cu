@@ -163,6 +163,22 @@ void make_plan(int n, int G, int r, ShardPlan &P)
             P.total_slots = acc;
         }
     }
+    // local tiles first (they are transferred while the shared ones are exchanged), each
+    // group in ascending global tile id
+    std::vector<int> tl, il, ts, is;
+    for (size_t t = 0; t < P.tiles.size(); t++) {
+        if ((P.tinfo[t] & 3) == 0) {
+            tl.push_back(P.tiles[t]);
+            il.push_back(P.tinfo[t]);
+        } else {
+            ts.push_back(P.tiles[t]);
+            is.push_back(P.tinfo[t]);
+        }
+    }
+    tl.insert(tl.end(), ts.begin(), ts.end());
+    il.insert(il.end(), is.begin(), is.end());
+    P.tiles.swap(tl);
+    P.tinfo.swap(il);
 }
 
 #ifdef QAP_HAVE_NCCL

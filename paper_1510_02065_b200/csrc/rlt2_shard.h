@@ -27,7 +27,7 @@ struct ShardPlan {
     std::vector<int64_t> blk_lo;   // G+1: rank-major offsets: rank q's blocks are S_rm[blk_lo[q], blk_lo[q+1])
     std::vector<int64_t> pos_off;  // n: rank-major position of global block b of facility f = b + pos_off[f]
     std::vector<int64_t> loc_off;  // n: local index of global block b of a facility f owned here = b + loc_off[f]
-    std::vector<int> tiles;        // this rank's tiles (global id), ascending
+    std::vector<int> tiles;        // this rank's tiles (global id): the n_local local ones, then the shared; each ascending
     std::vector<int> tinfo;        // kind | slot << 2
     std::vector<int64_t> peer_slots, peer_off;  // G: exchanged tiles per peer, slot offset
     int64_t total_slots = 0;

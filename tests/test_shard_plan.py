@@ -48,7 +48,12 @@ def test_plan_partition_and_tiles(pkg, n, G):
     # every tile appears on the owner of its facility i and of its facility k
     seen = {}
     for r, p in enumerate(plans):
-        assert (np.diff(p["tiles"]) > 0).all(), "ascending global tile ids"
+        # the local tiles first (transferred during the exchange), then the shared ones,
+        # each group in ascending global tile id
+        loc = p["kind"] == 0
+        nl = int(loc.sum())
+        assert loc[:nl].all() and not loc[nl:].any(), "local tiles first"
+        assert (np.diff(p["tiles"][:nl]) > 0).all() and (np.diff(p["tiles"][nl:]) > 0).all(), "ascending ids"
         for t, kind in zip(p["tiles"], p["kind"]):
             seen.setdefault(int(t), []).append((r, int(kind)))
     assert len(seen) == len(tri) * nt3
