@@ -1515,11 +1515,11 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     int64_t cap = (int64_t)num_sms * per_sm;
     if (a.sched) cap = (int64_t)num_sms * (per_sm < ctas_per_sm ? per_sm : ctas_per_sm);
     const int grid = (int)(want < cap ? want : cap);
-    // grabs of 4 blocks amortise the queue's atomics when every warp gets many LAPs; when the
-    // LAPs barely fill the resident warps (small B&B nodes) every warp should take one
+    // one block per queue grab: the grab's atomic is issued a whole LAP before its block is
+    // needed, and single grabs shorten the tail (N = 30: lap2 1.385 -> 1.372 ms, N = 20: 0.1925
+    // -> 0.188 ms against grabs of 4; one box, profiles/r02/README.md)
     LapArgs b = a;
-    const int64_t warps = (int64_t)grid * wpc;
-    b.chunk = a.count >= 8 * warps ? 4 : (a.count >= 3 * warps ? 2 : 1);
+    b.chunk = 1;
     k_lap<CPL><<<grid, 32 * wpc, smem, st>>>(b);
     return cudaGetLastError();
 }
