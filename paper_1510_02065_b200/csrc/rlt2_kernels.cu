@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "rlt2_internal.h"
@@ -1483,30 +1484,34 @@ cudaError_t launch_credit(const Geom &g, const double *S, const Offsets &pos, do
 }
 
 template <int CPL>
-static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
+static cudaError_t raise_smem_limit()
 {
-    const size_t smem = lap_warp_smem(a.m, CPL) * wpc;
     // The dynamic-smem limit is a process-wide attribute of the kernel: raise it once per
     // device to the opt-in maximum (setting it per launch to the exact size would race
     // between threads launching different sizes, e.g. concurrent B&B workers).
     static std::mutex mu;
     static uint64_t done_dev = 0;
-    {
-        int dev = 0;
-        cudaError_t e0 = cudaGetDevice(&dev);
-        if (e0 != cudaSuccess) return e0;
-        std::lock_guard<std::mutex> lk(mu);
-        if (dev >= 64 || !((done_dev >> dev) & 1)) {
-            int mx = 0;
-            if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
-                return e0;
-            if ((e0 = cudaFuncSetAttribute(k_lap<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) != cudaSuccess)
-                return e0;
-            if (dev < 64) done_dev |= 1ull << dev;
-        }
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 64 || !((done_dev >> dev) & 1)) {
+        int mx = 0;
+        if ((e0 = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e0;
+        if ((e0 = cudaFuncSetAttribute(k_lap<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx)) != cudaSuccess)
+            return e0;
+        if (dev < 64) done_dev |= 1ull << dev;
     }
+    return cudaSuccess;
+}
+
+template <int CPL>
+static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int ctas_per_sm, cudaStream_t st)
+{
+    const size_t smem = lap_warp_smem(a.m, CPL) * wpc;
+    cudaError_t e = raise_smem_limit<CPL>();
+    if (e != cudaSuccess) return e;
     if (smem > 232448) return cudaErrorInvalidValue;
-    cudaError_t e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<CPL>, 32 * wpc, smem);
     if (e != cudaSuccess) return e;
@@ -1524,6 +1529,18 @@ static cudaError_t launch_lap_on(const LapArgs &a, int num_sms, int wpc, int cta
     return cudaGetLastError();
 }
 
+// c CTAs of k_lap<cpl> with `threads` threads and `smem` dynamic bytes resident per SM?  (The
+// occupancy calculator knows the register file's per-sub-partition allocation: 2 CTAs of 18
+// warps at 56 registers do not fit although 36 warps would.)
+static bool lap_fits(int cpl, int threads, size_t smem, int c)
+{
+    int per_sm = 0;
+    cudaError_t e = cpl == 1
+                        ? (raise_smem_limit<1>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<1>, threads, smem))
+                        : (raise_smem_limit<2>(), cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lap<2>, threads, smem));
+    return e == cudaSuccess && per_sm >= c;
+}
+
 // lap_cfg: bits 0-7 = warps per CTA (0: default), bits 12-15 = CTAs per SM in dynamic mode
 // (0: 1).
 static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cudaStream_t st)
@@ -1534,16 +1551,32 @@ static cudaError_t dispatch_lap(const LapArgs &a, int num_sms, int lap_cfg, cuda
     int cps = (lap_cfg >> 12) & 0xf;
     if (wpc <= 0 && a.sched) {
         // default level-2 configuration: the most resident warps per SM that shared memory
-        // allows (228 KB per SM, 1 KB reserved per CTA), e.g. 2 CTAs x 17 warps at m = 28
-        const size_t ws = lap_warp_smem(a.m, cpl);
-        int best = 0;
-        for (int c = 1; c <= 2; c++)
-            for (int w = 32; w >= 1; w--)
-                if ((size_t)c * (w * ws + 1024) <= 233472 && w * c <= 42 && w * c > best) {
-                    best = w * c;
-                    wpc = w;
-                    cps = c;
-                }
+        // (228 KB per SM, 1 KB reserved per CTA) and the register file allow, e.g. 2 CTAs x 17
+        // warps at m = 28; depends on (device, m) only, so searched once and cached.  (Round 2
+        // start: shared memory only, and up to 42 warps — at m = 18 that asked for 2 CTAs of 21
+        // warps, of which the registers hold one: 21 warps per SM instead of 36.)
+        static std::mutex mu;
+        static std::map<std::pair<int, int>, std::pair<int, int>> cache;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({dev, a.m});
+        if (it != cache.end()) {
+            wpc = it->second.first;
+            cps = it->second.second;
+        } else {
+            const size_t ws = lap_warp_smem(a.m, cpl);
+            int best = 0;
+            for (int c = 1; c <= 2; c++)
+                for (int w = 32; w >= 1; w--)
+                    if ((size_t)c * (w * ws + 1024) <= 233472 && w * c > best &&
+                        lap_fits(cpl, 32 * w, w * ws, c)) {
+                        best = w * c;
+                        wpc = w;
+                        cps = c;
+                    }
+            if (best > 0) cache[{dev, a.m}] = {wpc, cps};
+        }
     }
     if (wpc <= 0) wpc = a.sched ? 32 : 8;
     if (cps <= 0) cps = 1;

@@ -155,7 +155,7 @@ def test_config1_bound_n8_t20(orc, torch, pkg, family):
     o = st.bound(20, trace=True)
     assert g["lb_glb"] == o["lb_glb"]
     rel_close(g["trace"], o["trace"])
-    assert (g["trace"] == o["trace"]).all()
+    assert (np.asarray(g["trace"]) == np.asarray(o["trace"])).all()
     compare_state(pkg, h, st)
     assert g["lb"] <= de.brute_force_opt(inst.F, inst.D) * (1 + 1e-12)
     pkg.qap_destroy(h)
@@ -215,6 +215,31 @@ def test_config4_n30_full_state(orc, torch, pkg):
     assert gold["D_after_T"] == 2
     assert _group_digests(D, 30) == [x["blake2b"] for x in gold["D_groups"]]
     assert g["trace"].tolist() == [float(x) for x in gold["lb_trace"][:2]]
+
+
+@pytest.mark.parametrize("family,n", [("taib", 31), ("nug", 34)])
+def test_level2_full_state_m29_m32(orc, torch, pkg, family, n):
+    """m = n - 2 = 29 and 32 (the sizes of a tai35b-shaped B&B's first levels), in the launch
+    configuration the occupancy calculator picks for them: two iterations against the oracle run
+    live on all host cores — LB trace, B, C and the whole of D bit for bit."""
+    inst = qapgen.taib(n, 2) if family == "taib" else qapgen.nug(n, 2)
+    h = pkg.qap_rlt2_create(n, inst.F, inst.D)
+    g = pkg.qap_rlt2_bound(h, 2, trace=True)
+    B, C, D, lb = gpu_state(pkg, h, n)
+    pkg.qap_destroy(h)
+    orc.set_threads(os.cpu_count() or 1)
+    try:
+        st = orc.State(inst.F, inst.D)
+        o = st.bound(2, trace=True)
+    finally:
+        orc.set_threads(1)
+    assert g["lb_glb"] == o["lb_glb"]
+    assert (np.asarray(g["trace"]) == np.asarray(o["trace"])).all()
+    assert (B == st.B).all() and (C == st.C).all()
+    Dref = st.D
+    D = D.reshape(Dref.shape)
+    for a in range(0, Dref.shape[0], 65536):
+        assert (D[a:a + 65536] == Dref[a:a + 65536]).all()
 
 
 def test_config4_n30_T20_lb_trace(torch, pkg):
