@@ -1,7 +1,7 @@
 # usage: bash scripts/gpu_round2_final.sh <tag> : the round's evidence on one box — smoke, full GPU
 # suite, bench (N=30, all keys), reference arm, launch list, ncu --set full of lap2 (iteration 1)
 # and the transfer, lap2 instruction counts at iterations 1/5/10/20, bench lines at N=20/35/40,
-# compute-sanitizer memcheck/racecheck/synccheck on small workloads
+# (compute-sanitizer is closed on this pool: scripts/gpu_sanitize.sh for pools where it is not)
 cd $GRAFT_REPO_ROOT
 TAG=${1:-f}
 mkdir -p gpurun_out
@@ -19,11 +19,5 @@ for t in 1 5 10 20; do
 done
 for n in 20 35 40; do
   timeout 900 python bench.py --n $n --steps 3 --warmup 2 --no-cpu-baseline --no-bnb > gpurun_out/${TAG}_n$n.txt 2>&1
-done
-for tool in memcheck racecheck synccheck; do
-  extra=""
-  if [ $tool = synccheck ]; then extra="--num-cuda-barriers 65536"; fi
-  timeout 1200 compute-sanitizer --tool $tool $extra --error-exitcode 9 python scripts/sanitize_one.py > gpurun_out/${TAG}_sanitize_$tool.txt 2>&1
-  echo "$tool rc=$?" >> gpurun_out/${TAG}_sanitize_$tool.txt
 done
 tail -n 2 gpurun_out/${TAG}_bench.txt | cut -c1-300

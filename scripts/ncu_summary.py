@@ -42,8 +42,27 @@ if __name__ == "__main__":
             continue
         s = summarise(rep, k)
         json.dump(s, open(f"profiles/{rnd}/ncu_{k}.json", "w"), indent=1)
-        traffic[k] = {"dram_bytes_per_launch": s["dram_bytes_per_launch"],
+        traffic[k] = {"n": 30, "dram_bytes_per_launch": s["dram_bytes_per_launch"],
                       "inst_executed_per_launch": s["inst_executed"], "source": f"profiles/{rnd}/ncu_{k}.json",
                       "capture": f"{tag} ncu --set full, N=30 nug seed 1"}
+        if k == "lap2":  # warp instructions fall over the ascent: mean over iterations 1..20
+            by_it = {}
+            for t in (1, 5, 10, 20):
+                f = f"gpurun_out/{tag}_lap2_it{t}.csv"
+                if os.path.exists(f):
+                    for row in csv.reader(open(f)):
+                        if len(row) > 3 and row[-3] == "smsp__inst_executed.sum":
+                            by_it[t] = float(row[-1].replace(",", ""))
+            if len(by_it) == 4:
+                ts = sorted(by_it)
+                def interp(x):
+                    for a, b in zip(ts, ts[1:]):
+                        if a <= x <= b:
+                            return by_it[a] + (by_it[b] - by_it[a]) * (x - a) / (b - a)
+                mean = sum(interp(x) for x in range(1, 21)) / 20
+                traffic[k].update({"inst_executed_per_launch": mean, "inst_executed_iteration1": by_it[1],
+                                   "inst_executed_by_iteration": {str(t): by_it[t] for t in ts},
+                                   "inst_note": "mean over iterations 1..20 interpolated from ncu metric passes at "
+                                                f"1, 5, 10, 20 (gpurun_out/{tag}_lap2_it*.csv, copied to profiles/{rnd}/)"})
         print(k, json.dumps(s)[:600])
     json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
