@@ -70,9 +70,10 @@ struct qap_rlt2 {
     bool loopback = false;    // member of an in-process group: the group driver moves data
     ShardPlan plan;           // for the current n
     int *dTiles = nullptr, *dTinfo = nullptr;
-    // the transfer of the local tiles runs on sSide while the shared tiles are exchanged
-    cudaStream_t sSide = nullptr;
-    cudaEvent_t evFork = nullptr, evLocal = nullptr;
+    // the transfer of the local tiles runs on sSide while the shared tiles are exchanged, piece
+    // by piece on sComm (evPack: piece packed, evX: piece received)
+    cudaStream_t sSide = nullptr, sComm = nullptr;
+    cudaEvent_t evFork = nullptr, evLocal = nullptr, evPack[kXChunks] = {}, evX[kXChunks] = {};
     size_t tiles_cap = 0, slots_cap = 0;
     int64_t dblk_cap = 0;     // stored blocks the D allocation can hold
     double *dSend = nullptr, *dRecv = nullptr, *dSall = nullptr;
@@ -189,7 +190,12 @@ static void free_all(qap_rlt2 *h)
     cudaFree(h->dTinfo);
     if (h->evFork) cudaEventDestroy(h->evFork);
     if (h->evLocal) cudaEventDestroy(h->evLocal);
+    for (int c = 0; c < kXChunks; c++) {
+        if (h->evPack[c]) cudaEventDestroy(h->evPack[c]);
+        if (h->evX[c]) cudaEventDestroy(h->evX[c]);
+    }
     if (h->sSide) cudaStreamDestroy(h->sSide);
+    if (h->sComm) cudaStreamDestroy(h->sComm);
     cudaFree(h->dSend);
     cudaFree(h->dRecv);
     cudaFree(h->dSall);
@@ -329,7 +335,11 @@ static qap_status create_impl(int32_t N, const int64_t *F, const int64_t *D, con
         ALLOC(h->dSend, h->slots_cap * kSlot * 8 + 16);
         ALLOC(h->dRecv, h->slots_cap * kSlot * 8 + 16);
         ALLOC(h->dSall, (size_t)gN.nblk * 8 + 16);
-        if ((e = cudaStreamCreateWithFlags(&h->sSide, cudaStreamNonBlocking)) != cudaSuccess ||
+        for (int c = 0; c < kXChunks && e == cudaSuccess; c++)
+            if ((e = cudaEventCreateWithFlags(&h->evPack[c], cudaEventDisableTiming)) == cudaSuccess)
+                e = cudaEventCreateWithFlags(&h->evX[c], cudaEventDisableTiming);
+        if (e != cudaSuccess || (e = cudaStreamCreateWithFlags(&h->sSide, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&h->sComm, cudaStreamNonBlocking)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&h->evFork, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&h->evLocal, cudaEventDisableTiming)) != cudaSuccess) {
             free_all(h);
@@ -553,33 +563,47 @@ static cudaError_t run_shard_sub(qap_rlt2 *h, int phase, int sub, cudaStream_t s
     cudaError_t e = cudaSuccess;
     const Geom &g = h->geom;
     const ShardPlan &P = h->plan;
-    // the plan lists the local tiles first, then the shared ones (make_plan)
-    const int nloc = P.n_local, nsh = (int)P.tiles.size() - P.n_local;
+    // the plan lists the local tiles first, then the shared ones by exchange piece (make_plan)
+    const int nloc = P.n_local;
     if (phase == QAP_PHASE_TRANSFER && sub == 0) {
         e = launch(h, QAP_K_SIGMA, st, [&](cudaStream_t s) {
             return launch_sigma(g, h->dB, h->dC, h->dSigma, h->dCtl, h->dSched, s);
         });
         if (e) return e;
-        TransferArgs A = transfer_args(h);
-        A.pack = 1;  // pass 1: this side's partials of the shared tiles
-        A.tiles += nloc;
-        A.tinfo += nloc;
-        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, nsh, s); });
-        if (e || nloc == 0) return e;
-        // the local tiles need no exchange: transferred on the side stream while the caller
-        // exchanges the shared tiles' partials on `st` (joined in sub-phase 1); disjoint classes
+        // pass 1: this side's partials of the shared tiles, piece by piece (evPack[c]: piece c
+        // may go on the wire)
+        for (int c = 0; c < kXChunks; c++) {
+            TransferArgs A = transfer_args(h);
+            A.pack = 1;
+            A.tiles += nloc + P.piece_lo[c];
+            A.tinfo += nloc + P.piece_lo[c];
+            const int cnt = P.piece_lo[c + 1] - P.piece_lo[c];
+            if (cnt > 0 &&
+                (e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, cnt, s); })) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(h->evPack[c], st)) != cudaSuccess) return e;
+        }
+        if (nloc == 0) return e;
+        // the local tiles need no exchange: transferred on the side stream while the shared
+        // tiles' partials are exchanged (joined in sub-phase 1); disjoint classes
         if ((e = cudaEventRecord(h->evFork, st)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(h->sSide, h->evFork, 0)) != cudaSuccess)
             return e;
         TransferArgs L = transfer_args(h);
         e = launch(h, QAP_K_TRANSFER, h->sSide, [&](cudaStream_t s) { return launch_transfer(L, nloc, s); });
         if (e == cudaSuccess) e = cudaEventRecord(h->evLocal, h->sSide);
-    } else if (phase == QAP_PHASE_TRANSFER && sub == 1) {
+    } else if (phase == QAP_PHASE_TRANSFER && (sub == 1 || sub >= 16)) {
+        // pass 2: the class means of the shared tiles — piece sub - 16 once it has arrived
+        // (evX), or every piece (sub = 1: the caller moved all of them)
+        const int c0 = sub == 1 ? 0 : sub - 16, c1 = sub == 1 ? kXChunks : c0 + 1;
+        if (sub >= 16 && (e = cudaStreamWaitEvent(st, h->evX[c0], 0)) != cudaSuccess) return e;
+        TransferArgs A = transfer_args(h);
+        A.tiles += nloc + P.piece_lo[c0];
+        A.tinfo += nloc + P.piece_lo[c0];
+        const int cnt = P.piece_lo[c1] - P.piece_lo[c0];
+        if (cnt > 0) e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, cnt, s); });
+        if (e != cudaSuccess || (sub >= 16 && c1 < kXChunks)) return e;
         if (nloc > 0 && (e = cudaStreamWaitEvent(st, h->evLocal, 0)) != cudaSuccess) return e;
-        TransferArgs A = transfer_args(h);  // pass 2: the class means of the shared tiles
-        A.tiles += nloc;
-        A.tinfo += nloc;
-        e = launch(h, QAP_K_TRANSFER, st, [&](cudaStream_t s) { return launch_transfer(A, nsh, s); });
         h->d_zero = 0;
         h->b_zero = h->c_zero = 1;
     } else if (phase == QAP_PHASE_CONC_D && sub == 0) {
@@ -654,9 +678,19 @@ static cudaError_t run_phase(qap_rlt2 *h, int phase, cudaStream_t st, bool fused
         const int p0 = phase, p1 = fused ? QAP_PHASE_CONC_D : phase;
         for (int ph = p0; ph <= p1; ph++) {
             if ((e = run_shard_sub(h, ph, 0, st)) != cudaSuccess) return e;
-            e = ph == QAP_PHASE_TRANSFER ? h->tp->exchange(h->plan, h->dSend, h->dRecv, st)
-                                         : h->tp->allgather(h->plan, h->dSall, st);
-            if (e != cudaSuccess) return e;
+            if (ph == QAP_PHASE_TRANSFER) {
+                // piece c goes on the wire (sComm) once packed; its means are applied (st) once
+                // it has arrived, while the next piece is exchanged
+                for (int c = 0; c < kXChunks; c++) {
+                    if ((e = cudaStreamWaitEvent(h->sComm, h->evPack[c], 0)) != cudaSuccess ||
+                        (e = h->tp->exchange(h->plan, h->dSend, h->dRecv, c, h->sComm)) != cudaSuccess ||
+                        (e = cudaEventRecord(h->evX[c], h->sComm)) != cudaSuccess ||
+                        (e = run_shard_sub(h, ph, 16 + c, st)) != cudaSuccess)
+                        return e;
+                }
+                continue;
+            }
+            if ((e = h->tp->allgather(h->plan, h->dSall, st)) != cudaSuccess) return e;
             if ((e = run_shard_sub(h, ph, 1, st)) != cudaSuccess) return e;
         }
         return cudaSuccess;

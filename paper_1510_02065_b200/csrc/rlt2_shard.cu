@@ -40,26 +40,32 @@ struct HostTransport : Transport {
         if (e == cudaSuccess) cap = n;
         return e;
     }
-    cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, cudaStream_t st) override
+    cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, int piece, cudaStream_t st) override
     {
         const size_t tot = (size_t)P.total_slots * kSlot;
         if (tot == 0) return cudaSuccess;
         cudaError_t e = grow(tot);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hsend, send, tot * 8, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return e;
         off.assign(P.G, 0);
         cnt.assign(P.G, 0);
         for (int q = 0; q < P.G; q++) {
             if (q == P.r) continue;
-            off[q] = P.peer_off[q] * kSlot;
-            cnt[q] = P.peer_slots[q] * kSlot;
+            const int64_t a = xchunk_lo(P.peer_slots[q], piece), b = xchunk_lo(P.peer_slots[q], piece + 1);
+            off[q] = (P.peer_off[q] + a) * kSlot;
+            cnt[q] = (b - a) * kSlot;
+            if (cnt[q] && (e = cudaMemcpyAsync(hsend + off[q], send + off[q], cnt[q] * 8, cudaMemcpyDeviceToHost, st)) !=
+                              cudaSuccess)
+                return e;
         }
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
         if (cb.exchange(cb.ctx, hsend, hrecv, off.data(), cnt.data(), world, rank) != 0) {
             err = "host transport: exchange callback failed";
             return cudaErrorUnknown;
         }
-        if ((e = cudaMemcpyAsync(recv, hrecv, tot * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+        for (int q = 0; q < P.G; q++)
+            if (cnt[q] &&
+                (e = cudaMemcpyAsync(recv + off[q], hrecv + off[q], cnt[q] * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+                return e;
         return cudaStreamSynchronize(st);
     }
     cudaError_t allgather(const ShardPlan &P, double *S_all, cudaStream_t st) override
@@ -163,20 +169,32 @@ void make_plan(int n, int G, int r, ShardPlan &P)
             P.total_slots = acc;
         }
     }
-    // local tiles first (they are transferred while the shared ones are exchanged), each
-    // group in ascending global tile id
-    std::vector<int> tl, il, ts, is;
+    // local tiles first (they are transferred while the shared ones are exchanged), then the
+    // shared ones by exchange piece; ascending global tile id within each group
+    std::vector<int> tl, il;
+    std::vector<std::vector<int>> ts(kXChunks), is(kXChunks);
     for (size_t t = 0; t < P.tiles.size(); t++) {
         if ((P.tinfo[t] & 3) == 0) {
             tl.push_back(P.tiles[t]);
             il.push_back(P.tinfo[t]);
-        } else {
-            ts.push_back(P.tiles[t]);
-            is.push_back(P.tinfo[t]);
+            continue;
         }
+        // the tile's slot relative to its peer's range -> its piece
+        const int64_t slot = P.tinfo[t] >> 2;
+        int q = 0;
+        while (!(slot >= P.peer_off[q] && slot < P.peer_off[q] + P.peer_slots[q])) q++;
+        const int64_t rel = slot - P.peer_off[q];
+        int c = 0;
+        while (c + 1 < kXChunks && rel >= xchunk_lo(P.peer_slots[q], c + 1)) c++;
+        ts[c].push_back(P.tiles[t]);
+        is[c].push_back(P.tinfo[t]);
     }
-    tl.insert(tl.end(), ts.begin(), ts.end());
-    il.insert(il.end(), is.begin(), is.end());
+    P.piece_lo[0] = 0;
+    for (int c = 0; c < kXChunks; c++) {
+        tl.insert(tl.end(), ts[c].begin(), ts[c].end());
+        il.insert(il.end(), is[c].begin(), is[c].end());
+        P.piece_lo[c + 1] = P.piece_lo[c] + (int)ts[c].size();
+    }
     P.tiles.swap(tl);
     P.tinfo.swap(il);
 }
@@ -238,14 +256,15 @@ struct NcclTransport : Transport {
         err = std::string("NCCL: ") + g_nccl.errStr(r);
         return cudaErrorUnknown;
     }
-    cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, cudaStream_t st) override
+    cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, int piece, cudaStream_t st) override
     {
         ncclResult_t r;
         if ((r = g_nccl.groupStart()) != ncclSuccess) return fail(r);
         for (int q = 0; q < P.G; q++) {
-            if (q == P.r || P.peer_slots[q] == 0) continue;
-            const size_t cnt = (size_t)P.peer_slots[q] * kSlot;
-            const size_t off = (size_t)P.peer_off[q] * kSlot;
+            const int64_t a = xchunk_lo(P.peer_slots[q], piece), b = xchunk_lo(P.peer_slots[q], piece + 1);
+            if (q == P.r || b == a) continue;
+            const size_t cnt = (size_t)(b - a) * kSlot;
+            const size_t off = (size_t)(P.peer_off[q] + a) * kSlot;
             if ((r = g_nccl.send(send + off, cnt, ncclFloat64, q, comm, st)) != ncclSuccess) return fail(r);
             if ((r = g_nccl.recv(recv + off, cnt, ncclFloat64, q, comm, st)) != ncclSuccess) return fail(r);
         }

@@ -20,6 +20,11 @@
 namespace rlt2 {
 
 constexpr int kSlot = TT * TT * TT;  // doubles per exchanged tile (one per class slot)
+// The shared tiles are exchanged in kXChunks pieces (pack piece c+1 / apply piece c-1 while piece c
+// is on the wire): piece c of the slots a rank pair shares is [floor(c S / K), floor((c+1) S / K))
+// of their S common slots, the same range on both sides.
+constexpr int kXChunks = 4;
+inline int64_t xchunk_lo(int64_t slots, int c) { return slots * c / kXChunks; }
 
 struct ShardPlan {
     int n = 0, G = 1, r = 0;
@@ -27,11 +32,13 @@ struct ShardPlan {
     std::vector<int64_t> blk_lo;   // G+1: rank-major offsets: rank q's blocks are S_rm[blk_lo[q], blk_lo[q+1])
     std::vector<int64_t> pos_off;  // n: rank-major position of global block b of facility f = b + pos_off[f]
     std::vector<int64_t> loc_off;  // n: local index of global block b of a facility f owned here = b + loc_off[f]
-    std::vector<int> tiles;        // this rank's tiles (global id): the n_local local ones, then the shared; each ascending
+    std::vector<int> tiles;        // this rank's tiles (global id): the n_local local ones (ascending), then
+                                   // the shared ones by exchange piece (ascending within a piece)
     std::vector<int> tinfo;        // kind | slot << 2
     std::vector<int64_t> peer_slots, peer_off;  // G: exchanged tiles per peer, slot offset
     int64_t total_slots = 0;
     int n_local = 0, n_agg = 0, n_hold = 0;
+    int piece_lo[kXChunks + 1] = {0};  // shared tiles of piece c: tiles[n_local + piece_lo[c] .. n_local + piece_lo[c+1])
 };
 
 // Partition + tile lists of rank r among G for the reduced size n.
@@ -40,8 +47,9 @@ void make_plan(int n, int G, int r, ShardPlan &P);
 // Collective transport between the ranks of one sharded bound.
 struct Transport {
     virtual ~Transport() {}
-    // send[peer_off[s]*kSlot .. + peer_slots[s]*kSlot) to s, receive the same range of recv from s
-    virtual cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, cudaStream_t st) = 0;
+    // piece c (xchunk_lo) of send[peer_off[s]*kSlot .. + peer_slots[s]*kSlot) to every peer s,
+    // the same range of recv from s; enqueued on st (the host transport returns when it is done)
+    virtual cudaError_t exchange(const ShardPlan &P, const double *send, double *recv, int piece, cudaStream_t st) = 0;
     // S_all[blk_lo[q] .. blk_lo[q+1]) of rank q -> every rank (in place)
     virtual cudaError_t allgather(const ShardPlan &P, double *S_all, cudaStream_t st) = 0;
     virtual const char *error() const = 0;

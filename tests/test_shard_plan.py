@@ -48,12 +48,25 @@ def test_plan_partition_and_tiles(pkg, n, G):
     # every tile appears on the owner of its facility i and of its facility k
     seen = {}
     for r, p in enumerate(plans):
-        # the local tiles first (transferred during the exchange), then the shared ones,
-        # each group in ascending global tile id
+        # the local tiles first (transferred during the exchange), then the shared ones by
+        # exchange piece c: slot s of the S slots shared with peer q (range starting at off_q)
+        # lies in piece c when floor(c S / 4) <= s - off_q < floor((c + 1) S / 4); ascending
+        # global tile id within each group
         loc = p["kind"] == 0
         nl = int(loc.sum())
         assert loc[:nl].all() and not loc[nl:].any(), "local tiles first"
-        assert (np.diff(p["tiles"][:nl]) > 0).all() and (np.diff(p["tiles"][nl:]) > 0).all(), "ascending ids"
+        assert (np.diff(p["tiles"][:nl]) > 0).all(), "local tiles ascending"
+        off = np.concatenate([[0], np.cumsum(p["peer_slots"])])
+        pieces = []
+        for s in p["slot"][nl:]:
+            q = int(np.searchsorted(off, s, side="right") - 1)
+            S, rel = int(p["peer_slots"][q]), int(s - off[q])
+            pieces.append(max(c for c in range(4) if S * c // 4 <= rel))
+        pieces = np.array(pieces, np.int64)
+        assert (np.diff(pieces) >= 0).all(), "shared tiles ordered by exchange piece"
+        for c in range(4):
+            t = p["tiles"][nl:][pieces == c]
+            assert (np.diff(t) > 0).all(), "ascending within a piece"
         for t, kind in zip(p["tiles"], p["kind"]):
             seen.setdefault(int(t), []).append((r, int(kind)))
     assert len(seen) == len(tri) * nt3
