@@ -181,8 +181,8 @@ void make_plan(int n, int G, int r, ShardPlan &P)
         }
         // the tile's slot relative to its peer's range -> its piece
         const int64_t slot = P.tinfo[t] >> 2;
-        int q = 0;
-        while (!(slot >= P.peer_off[q] && slot < P.peer_off[q] + P.peer_slots[q])) q++;
+        int q = 0;  // the peer whose slot range holds it (every shared tile has one)
+        while (q + 1 < G && !(slot >= P.peer_off[q] && slot < P.peer_off[q] + P.peer_slots[q])) q++;
         const int64_t rel = slot - P.peer_off[q];
         int c = 0;
         while (c + 1 < kXChunks && rel >= xchunk_lo(P.peer_slots[q], c + 1)) c++;
