@@ -2,7 +2,7 @@
 # travels with the snapshot) and is copied back through gpurun_out/
 cd $GRAFT_REPO_ROOT
 TAG=${1:-j1d}
-B=${2:-3600}
+B=${2:-3200}
 mkdir -p gpurun_out/j1_ckpt
 cp profiles/r02/bnb/j1_ckpt/* gpurun_out/j1_ckpt/ 2>/dev/null
 R=""; [ -f gpurun_out/j1_ckpt/taib35.ckpt ] && R="--resume"
